@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Onesweep B200 benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 runs BASELINE.json configs[1] (C2): 256M uniform u32 keys, keys only,
+8-bit digits (1 histogram + 4 chained-scan binning passes).  N>1 runs the
+sharded sort (MSD top-digit split + NCCL all-to-all + local Onesweep) with
+256M keys per rank (weak scaling; N=8 is C5's 2^31 keys).
+
+A "step" is one full sort of the resident input.  Inputs are 1 GiB per GPU,
+far larger than the 126 MB L2, so no flush is needed between steps.
+`--impl reference` times the CPU port of the reference algorithm
+(oracle/liboracle.so, C restatement of onesweep_sort) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_A100_GKEYS = 29.4  # PAPER.md:17, 256M random u32 keys-only
+N_PER_GPU = 1 << 28
+
+
+def _baseline_metric() -> str:
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:  # pragma: no cover
+        return "GKey/s sorting 256M random uint32 keys; % of HBM roofline (~(1+2p)n words)"
+
+
+def _peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _ncu_traffic() -> dict:
+    """Per-launch DRAM bytes of each kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {
+        "hw_slowdown": 0x8,
+        "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80,
+        "sw_power_cap": 0x4,
+        "sync_boost": 0x10,
+    }
+
+    def __init__(self, index: int):
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((mhz, reasons))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        seen = 0
+        for _, r in self.samples:
+            seen |= r
+        names = [k for k, bit in self.REASONS.items() if seen & bit]
+        return {
+            "sm_mhz": statistics.median(m for m, _ in self.samples),
+            "sm_max_mhz": self.max_mhz,
+            "reasons": names,
+            "samples": len(self.samples),
+        }
+
+
+def cpu_port_sort(n: int, threads: int, seed: int = 0) -> tuple[float, dict]:
+    """Time the oracle's C port of the reference onesweep_sort on the host."""
+    from oracle import oracle
+
+    keys = oracle.keygen(n, 1, seed)
+    oracle.sort(keys[: 1 << 16], tile=4096, threads=threads)  # warm the pages / threads
+    t0 = time.perf_counter()
+    out = oracle.sort(keys, tile=4096, threads=threads)
+    dt = time.perf_counter() - t0
+    assert out.size == n
+    return dt, {"n": n}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = args.cpu_sample
+    for _ in range(args.warmup):
+        cpu_port_sort(n, threads)
+    times = [cpu_port_sort(n, threads)[0] for _ in range(args.steps)]
+    t = statistics.mean(times)
+    value = n / t / 1e9
+    sample = (f"2^{n.bit_length() - 1} uniform u32 keys-only (keygen q=1 seed=0) per step, "
+              f"d=8, tile 4096 (reference default), {threads} threads")
+    line = {
+        "impl": "reference",
+        "metric": _baseline_metric(),
+        "value": value,
+        "unit": "GKey/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": value / PAPER_A100_GKEYS,
+        "dtype": "u32",
+        "data": "synthetic (reference keygen, q=1, seed 0)",
+        "config": {"workload": "C2 sample: uniform u32 keys-only, 8-bit digits, CPU port of the "
+                               "reference onesweep_sort (oracle/onesweep_oracle.c)", "n": n},
+        "cpu_baseline": {"value": value, "unit": "GKey/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GKey/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2206_01784_b200 import DeviceSorter, KeyGenSpec, generate_keys, _native, onesweep_sort
+
+    n = args.n
+    keys = generate_keys(KeyGenSpec(q=1, seed=0, n=n), device=dev, first_index=rank * n)
+    out = torch.empty_like(keys)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if world == 1:
+        sorter = DeviceSorter(n, torch.uint32, 0, 8, device=dev)
+        passes = sorter.passes
+        strips = -(-n // (1 << 28))
+        launches_per_step = 1 + passes * strips
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(passes + 2)]
+              for _ in range(args.steps)]
+        L = _native.load()
+        for row in ev:  # torch creates CUDA events lazily; force the handles now
+            for e in row:
+                e.record(stream)
+
+        def step(i=None):
+            if i is None:
+                sorter(keys, out, stats=False)
+                return
+            handles = (_native._vp * (passes + 2))(*[e.cuda_event for e in ev[i]])
+            _native.check(L.os_sort_events(
+                keys.data_ptr(), out.data_ptr(), None, None, n, 0, 0, 8, 0, 32, sorter.tile,
+                0, sorter.ws.data_ptr(), sorter.ws.numel(), None, handles, passes + 2,
+                stream.cuda_stream), "os_sort_events")
+    else:
+        from paper_2206_01784_b200.distributed import ShardedSorter
+
+        sorter = ShardedSorter(n, torch.uint32, device=dev)
+        passes = sorter.local_passes
+        launches_per_step = sorter.launches_per_step
+        ev = None
+
+        def step(i=None):
+            sorter(keys)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t_end.record(stream)
+        barrier()
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    ms = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item())
+    total_keys = n * world
+    value = total_keys / (ms_per_step * 1e-3) / 1e9
+
+    peaks = _peaks()
+    kb = 4
+    alg_bytes = (1 + 2 * passes) * n * kb
+    line = {
+        "metric": _baseline_metric(),
+        "value": value,
+        "unit": "GKey/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": value / PAPER_A100_GKEYS,
+        "vs_baseline_ref": "29.4 GKey/s, A100-80GB (PAPER.md:17; BASELINE.md section 1)",
+        "dtype": "u32",
+        "data": "synthetic: reference keygen (q=1, seed 0) restated on device, bit-identical",
+        "config": {
+            "workload": ("C2: 256M uniform u32 keys-only, 8-bit digits, 1 histogram + 4 binning passes"
+                         if world == 1 else
+                         f"C5-style sharded sort: {n} u32 keys per GPU, MSD split + NCCL all-to-all "
+                         "+ local Onesweep"),
+            "n_per_gpu": n,
+            "digit_bits": 8,
+            "tile_keys": getattr(sorter, "tile", None),
+            "parallelism": f"dp{world}" if world > 1 else "single",
+            "l2": "1 GiB inputs per GPU > 126 MB L2: no flush between steps",
+        },
+        "hbm_roofline_frac_sort": (alg_bytes / (ms_local * 1e-3) / 1e9) / peaks["hbm_gbs"],
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+    if world == 1:
+        torch.cuda.synchronize()
+        hist_us = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)) * 1e3
+        pass_us = [statistics.mean(ev[i][1 + k].elapsed_time(ev[i][2 + k]) for i in range(args.steps)) * 1e3
+                   for k in range(passes)]
+        bin_us = statistics.mean(pass_us)
+        bin_bytes = 2 * n * kb
+        achieved = bin_bytes / (bin_us * 1e-6) / 1e9
+        traffic = _ncu_traffic().get("binning")
+        line["roofline"] = {
+            "kernel": "onesweep_binning_kernel",
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peaks["hbm_gbs"],
+            "peak_source": peaks["source"],
+            "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"],
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": bin_bytes,
+            "launch_us": bin_us,
+        }
+        line["kernels"] = {
+            "histogram_us": hist_us,
+            "histogram_gbs": n * kb / (hist_us * 1e-6) / 1e9,
+            "binning_pass_us": pass_us,
+            "share_binning": sum(pass_us) / (ms_per_step * 1e3),
+        }
+        # correctness spot check of the timed output (cheap, outside timing)
+        o = out[: 1 << 20].cpu().numpy()
+        line["output_sorted_prefix"] = bool((o[1:] >= o[:-1]).all())
+
+        # e2e: public API, host (pinned) buffers in, host array out, per step
+        if args.e2e_steps > 0:
+            keys_h = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+            keys_h.copy_(keys)
+            keys_np = keys_h.numpy()
+            e2e_times = []
+            for _ in range(args.e2e_steps + 1):  # first call is the warm-up
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = onesweep_sort(keys_np)
+                t1 = time.perf_counter()
+                e2e_times.append(t1 - t0)
+                del res
+            e2e_t = statistics.mean(e2e_times[1:])
+            line["e2e"] = {"value": n / e2e_t / 1e9, "unit": "GKey/s", "h2d_bytes_per_step": n * kb,
+                           "d2h_bytes_per_step": n * kb, "ms_per_step": e2e_t * 1e3,
+                           "api": "paper_2206_01784_b200.onesweep_sort(numpy view of pinned host memory)"}
+            del keys_h, keys_np
+        if args.cpu_baseline and rank == 0:
+            threads = os.cpu_count() or 1
+            dt, _ = cpu_port_sort(args.cpu_sample, threads)
+            line["cpu_baseline"] = {
+                "value": args.cpu_sample / dt / 1e9, "unit": "GKey/s", "cores": threads,
+                "kind": "port",
+                "sample": f"2^{args.cpu_sample.bit_length() - 1} keys of the C2 distribution "
+                          "(keygen q=1 seed 0), C port of reference onesweep_sort, tile 4096, one run",
+            }
+    else:
+        line["e2e"] = sorter.e2e_line(keys, args.e2e_steps) if hasattr(sorter, "e2e_line") else None
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("timing rules need >= 3 warm-up steps")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

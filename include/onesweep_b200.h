@@ -1,0 +1,177 @@
+/*
+ * onesweep_b200.h -- C ABI of the B200-native Onesweep radix sort.
+ *
+ * This is the drop-in boundary for the reference package `onesweep`
+ * (/root/reference/pkg/src/onesweep).  The reference keeps every hot loop in
+ * four numba kernels (_kernels.py:3-6) called from thin Python wrappers; this
+ * library replaces those loops *and* the tile scheduling around them
+ * (executor.py:160-212, lookback.py:127-169) with sm_100a CUDA kernels.
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument that names array data is a DEVICE pointer,
+ *     caller-owned; the library never allocates device memory;
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream);
+ *   - return value is an os_status; os_last_error() gives a message for the
+ *     calling thread;
+ *   - calls are reentrant on distinct workspaces, not on a shared one.
+ *
+ * Status codes map onto the reference's exception classes:
+ *   OS_ERR_ARG      -> ValueError   (binning.py:295-304, keycodec.py:107-123)
+ *   OS_ERR_KEYTYPE  -> KeyError     (keycodec.py:70-85)
+ *   OS_ERR_CUDA     -> RuntimeError
+ */
+#ifndef ONESWEEP_B200_H
+#define ONESWEEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum os_status {
+  OS_OK = 0,
+  OS_ERR_ARG = 1,
+  OS_ERR_KEYTYPE = 2,
+  OS_ERR_CUDA = 3,
+  OS_ERR_WORKSPACE = 4
+} os_status;
+
+/* Key types, same set and names as keycodec.KEY_TYPES (keycodec.py:55-65). */
+typedef enum os_key_type {
+  OS_KEY_U32 = 0,
+  OS_KEY_U64 = 1,
+  OS_KEY_I32 = 2,
+  OS_KEY_I64 = 3,
+  OS_KEY_F32 = 4,
+  OS_KEY_F64 = 5
+} os_key_type;
+
+/* Order-preserving codecs applied on load / store by the kernels
+ * (keycodec.py:157-181). */
+typedef enum os_codec {
+  OS_CODEC_NONE = 0,       /* unsigned keys, or already-encoded bits     */
+  OS_CODEC_SIGNED = 1,     /* x ^ sign  (its own inverse)                */
+  OS_CODEC_FLOAT_ENC = 2,  /* neg ? ~x : x | sign                        */
+  OS_CODEC_FLOAT_DEC = 3   /* (x & sign) ? x ^ sign : ~x                 */
+} os_codec;
+
+/* Device-side statistics, filled with atomics when a non-NULL pointer is
+ * passed (mirrors executor.LedgerCounts' schedule-dependent columns). */
+typedef struct os_device_stats {
+  unsigned long long fast_path_tiles; /* short-circuit tiles (binning.py:201-205) */
+  unsigned long long lookback_reads;  /* status words read in look-back (lookback.py:144-169) */
+  unsigned long long tiles;           /* tiles processed */
+} os_device_stats;
+
+const char* os_version(void);
+const char* os_last_error(void);
+
+/* Largest digit width the binning kernel supports natively (radix <= 256). */
+int os_max_digit_bits(void);
+
+/* Default device tile (keys per thread block) for this key/value width;
+ * the kernels accept any tile_keys in [1, os_tile_capacity]. */
+int os_tile_capacity(int key_bytes, int val_bytes);
+
+/* ---- elementwise ---------------------------------------------------------
+ * encode_array / decode_array (keycodec.py:184-212) on device memory. */
+int os_encode(const void* in, void* out, size_t n, int key_type, void* stream);
+int os_decode(const void* in, void* out, size_t n, int key_type, void* stream);
+
+/* Device restatement of keygen.generate_keys (keygen.py:46-76): key i (for
+ * i = first_index .. first_index+n-1) is the AND of splitmix64 words at
+ * counters i*q .. i*q+q-1, truncated to key_bits.  Bit-identical. */
+int os_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
+              unsigned long long first_index, void* stream);
+
+/* ---- upfront histogram (histogram.py:57-99) ---------------------------
+ * Reads keys once and counts the digit at every place for bits
+ * [begin_bit, end_bit) of the *encoded* key (codec applied on load).
+ * hist_out:    u64[passes][radix], overwritten (not accumulated).
+ * offsets_out: u64[passes][radix] exclusive sums per place, or NULL.
+ * passes = ceil((end_bit - begin_bit) / digit_bits).
+ * workspace:   os_histogram_workspace_bytes() bytes (zeroed by the call). */
+size_t os_histogram_workspace_bytes(void);
+int os_histogram(const void* keys, size_t n, int key_bytes, int codec, int digit_bits,
+                 int begin_bit, int end_bit, unsigned long long* hist_out,
+                 unsigned long long* offsets_out, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* Per-row exclusive prefix sum of a u64[rows][radix] table
+ * (histogram.exclusive_sum / global_bin_offsets, histogram.py:49-54,94-99). */
+int os_exclusive_scan(const unsigned long long* counts, int rows, int radix,
+                      unsigned long long* offsets_out, void* stream);
+
+/* ---- one chained-scan binning pass (binning.py:218-275) ----------------
+ * Stable 2^digit_width-way partition of src into dst by
+ * (key >> shift) & (2^digit_width - 1) of the encoded key.
+ * base_offsets: device u64[radix] -- a bin-offset row or a StripCarry.
+ * carry_out:    device u64[radix] -- receives base + per-digit totals
+ *               (StripCarry semantics); may alias nothing else.
+ * Keys are processed in strips of <= strip_keys (binning.py:241-246) and
+ * tiles of tile_keys (<= os_tile_capacity); status words follow the
+ * reference's CounterMatrix layout (lookback.py:33-79): u32[tiles][radix],
+ * bits 31-30 status {N,L,G}, bits 29-0 value.
+ * status_out: optional device u32 buffer of os_partition_status_words()
+ *             words that receives the final status words of every strip
+ *             (tile-major, strips concatenated); NULL = internal.
+ * workspace: os_partition_workspace_bytes() bytes. */
+size_t os_partition_status_words(size_t n, int digit_width, int tile_keys, size_t strip_keys);
+size_t os_partition_workspace_bytes(size_t n, int digit_width, int tile_keys,
+                                    size_t strip_keys);
+int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals,
+                      void* dst_vals, size_t n, int key_bytes, int val_bytes, int shift,
+                      int digit_width, const unsigned long long* base_offsets,
+                      unsigned long long* carry_out, int codec_in, int codec_out,
+                      int tile_keys, size_t strip_keys, unsigned int* status_out,
+                      void* workspace, size_t workspace_bytes, os_device_stats* stats,
+                      void* stream);
+
+/* ---- the whole sort (binning.py:278-337) --------------------------------
+ * keys_in / vals_in are never written.  keys_out / vals_out receive the
+ * stably sorted keys (native bit pattern) and their values.  vals_* may be
+ * NULL (keys only; val_bytes must then be 0).  digit_bits <= 8.
+ * tile_keys = 0 selects os_tile_capacity; strip_keys = 0 selects 2^28. */
+size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_bits,
+                               int begin_bit, int end_bit, int tile_keys,
+                               size_t strip_keys);
+int os_sort(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+            size_t n, int key_type, int val_bytes, int digit_bits, int begin_bit,
+            int end_bit, int tile_keys, size_t strip_keys, void* workspace,
+            size_t workspace_bytes, os_device_stats* stats, void* stream);
+
+/* Same as os_sort, and additionally records caller-created CUDA events
+ * (cudaEvent_t passed as void*) on `stream`: events[0] before the histogram,
+ * events[1] after it, events[2+k] after binning pass k.  num_events must be
+ * >= passes + 2.  Used by bench.py to time each kernel inside the timed
+ * region. */
+int os_sort_events(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                   size_t n, int key_type, int val_bytes, int digit_bits, int begin_bit,
+                   int end_bit, int tile_keys, size_t strip_keys, void* workspace,
+                   size_t workspace_bytes, os_device_stats* stats, void** events,
+                   int num_events, void* stream);
+
+/* ---- multi-GPU MSD splitter (no reference counterpart) -------
+ * Counts the top digit (bits [end_bit - digit_bits, end_bit) of the encoded
+ * key) into hist_out u64[2^digit_bits] (overwritten). */
+int os_msd_histogram(const void* keys, size_t n, int key_type, int digit_bits,
+                     int end_bit, unsigned long long* hist_out, void* stream);
+/* Stable partition of the local shard into `parts` contiguous destination
+ * segments: bins [bin_lo[g], bin_lo[g+1]) go to segment g.  bin_lo is a
+ * device u32[parts+1] with bin_lo[0]=0, bin_lo[parts]=radix; seg_offsets is a
+ * device u64[parts] of segment starts.  Keys/values keep their native bits. */
+size_t os_msd_partition_workspace_bytes(size_t n);
+int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in,
+                     void* vals_out, size_t n, int key_type, int val_bytes,
+                     int digit_bits, int end_bit, const unsigned int* bin_lo, int parts,
+                     const unsigned long long* seg_offsets, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ONESWEEP_B200_H */

@@ -1,0 +1,288 @@
+"""Onesweep sort and single partition passes, on the B200.
+
+Mirrors onesweep.binning (binning.py:1-337): `onesweep_sort` and
+`partition_pass` keep the reference's signatures, argument meaning, return
+types and exceptions; the per-tile pipeline (rank, publish, look-back,
+reorder, scatter) and the thread pool around it are replaced by one sm_100a
+kernel launch per digit place (csrc/binning.cu), after one upfront histogram
+launch (csrc/histogram.cu).
+
+Accepted inputs: numpy arrays (copied to the device and back: a drop-in for
+the reference) or CUDA torch tensors (zero-copy, result on the device).
+Additions over the reference: keyword-only `begin_bit` / `end_bit` (bits of
+the *encoded* key, CUB convention) and `stream`.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._device import as_device, from_device, is_tensor, workspace
+from .executor import Executor
+from .keycodec import MAX_DEVICE_DIGIT_BITS, RadixConfig, radix_plan, spec_for_dtype
+
+LANE_GROUP = 32
+
+
+@dataclass(frozen=True)
+class StripCarry:
+    """Per-digit 64-bit running global offsets chained between strips
+    (binning.py:88-92)."""
+
+    offsets: object  # uint64 numpy array or CUDA tensor, length radix
+
+
+@dataclass
+class SortBuffers:
+    """Ping-pong buffers (binning.py:95-131).  The device sort routes its
+    passes so that the last one lands in the output buffer, so no parity copy
+    is ever needed; this helper is kept for callers that drive passes
+    themselves."""
+
+    keys_a: object
+    keys_b: object
+    values_a: object | None = None
+    values_b: object | None = None
+    live_in_a: bool = True
+
+    @classmethod
+    def allocate(cls, encoded, values) -> "SortBuffers":
+        def empty_like(x):
+            if is_tensor(x):
+                import torch
+
+                return torch.empty_like(x)
+            return np.empty_like(x)
+
+        def copy(x):
+            return x.clone() if is_tensor(x) else x.copy()
+
+        return cls(
+            keys_a=encoded,
+            keys_b=empty_like(encoded),
+            values_a=None if values is None else copy(values),
+            values_b=None if values is None else empty_like(values),
+        )
+
+    def src_keys(self):
+        return self.keys_a if self.live_in_a else self.keys_b
+
+    def dst_keys(self):
+        return self.keys_b if self.live_in_a else self.keys_a
+
+    def src_values(self):
+        if self.values_a is None:
+            return None
+        return self.values_a if self.live_in_a else self.values_b
+
+    def dst_values(self):
+        if self.values_a is None:
+            return None
+        return self.values_b if self.live_in_a else self.values_a
+
+    def swap(self) -> None:
+        self.live_in_a = not self.live_in_a
+
+
+def _val_bytes(values) -> int:
+    if values is None:
+        return 0
+    vb = values.element_size() if is_tensor(values) else values.dtype.itemsize
+    if vb not in (1, 2, 4, 8):
+        raise ValueError(f"values must be 1, 2, 4 or 8 bytes wide, got {vb}")
+    return vb
+
+
+def _numel(x) -> int:
+    return x.numel() if is_tensor(x) else int(np.asarray(x).size)
+
+
+def _copy(x):
+    return x.clone() if is_tensor(x) else np.array(x, copy=True)
+
+
+def _device_digit_bits(cfg: RadixConfig) -> int:
+    # A stable LSD sort has one answer for every digit width, so wider
+    # configured digits run as 8-bit places on the device.
+    return min(cfg.digit_bits, MAX_DEVICE_DIGIT_BITS)
+
+
+class DeviceSorter:
+    """Pre-planned device sort of n keys (optionally with values).
+
+    Allocates the workspace once; `__call__` issues exactly one histogram and
+    `passes` binning launches on the stream, with no host synchronisation.
+    This is what bench.py times."""
+
+    def __init__(self, n: int, key_dtype, val_bytes: int = 0, digit_bits: int = 8,
+                 begin_bit: int = 0, end_bit: int | None = None, tile_size: int = 0,
+                 strip_size: int = 0, device=None):
+        import torch
+
+        self.spec = spec_for_dtype(key_dtype)
+        self.n = int(n)
+        self.val_bytes = int(val_bytes)
+        self.digit_bits = int(digit_bits)
+        self.begin_bit = int(begin_bit)
+        self.end_bit = self.spec.bits if end_bit is None else int(end_bit)
+        L = _native.load()
+        cap = L.os_tile_capacity(self.spec.bits // 8, self.val_bytes)
+        self.tile = min(int(tile_size), cap) if tile_size else cap
+        self.strip = int(strip_size)
+        self.passes = -(-(self.end_bit - self.begin_bit) // self.digit_bits)
+        nbytes = L.os_sort_workspace_bytes(self.n, self.spec.type_id, self.val_bytes,
+                                           self.digit_bits, self.begin_bit, self.end_bit,
+                                           self.tile, self.strip)
+        if self.n > 1 and nbytes == 0:
+            raise ValueError("invalid sort parameters: " + L.os_last_error().decode())
+        self.device = torch.device(device or "cuda")
+        self.ws = workspace(nbytes, self.device)
+        self.stats = torch.zeros(3, dtype=torch.int64, device=self.device)
+
+    def __call__(self, keys, keys_out, values=None, values_out=None, stream=None, stats=True):
+        _native.check(
+            _native.load().os_sort(
+                _native.ptr(keys), _native.ptr(keys_out), _native.ptr(values),
+                _native.ptr(values_out), self.n, self.spec.type_id, self.val_bytes,
+                self.digit_bits, self.begin_bit, self.end_bit, self.tile, self.strip,
+                _native.ptr(self.ws), self.ws.numel(),
+                _native.ptr(self.stats) if stats else None, _native.stream_handle(stream)),
+            "onesweep_sort",
+        )
+        return keys_out if values is None else (keys_out, values_out)
+
+
+def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
+                  executor: Executor | None = None, *, begin_bit: int = 0,
+                  end_bit: int | None = None, stream=None):
+    """Stable ascending sort (binning.py:278-337).
+
+    Returns the sorted keys, or (sorted keys, reordered values) when values
+    are given.  Inputs are never modified.  Same container type out as in."""
+    to_numpy = not is_tensor(keys)
+    if to_numpy:
+        keys = np.asarray(keys)
+    spec = spec_for_dtype(keys.dtype)  # KeyError for unsupported dtypes
+    if cfg is None:
+        cfg = radix_plan(spec.bits, 8)
+    elif cfg.key_bits != spec.bits:
+        raise ValueError(
+            f"config is for {cfg.key_bits}-bit keys but got {spec.bits}-bit {spec.name}"
+        )
+    if executor is None:
+        executor = Executor()
+    if values is not None:
+        if not is_tensor(values):
+            values = np.asarray(values)
+        if tuple(values.shape) != tuple(keys.shape):
+            raise ValueError("values must have the same length as keys")
+    end_bit = spec.bits if end_bit is None else int(end_bit)
+    if not 0 <= begin_bit < end_bit <= spec.bits:
+        raise ValueError(f"need 0 <= begin_bit < end_bit <= {spec.bits}, got [{begin_bit}, {end_bit})")
+    vb = _val_bytes(values)
+
+    n = _numel(keys)
+    if n <= 1:  # binning.py:306-309
+        sorted_keys = _copy(keys)
+        return sorted_keys if values is None else (sorted_keys, _copy(values))
+
+    import torch
+
+    dk, _ = as_device(keys)
+    dv = as_device(values)[0] if values is not None else None
+    ok = torch.empty_like(dk)
+    ov = torch.empty_like(dv) if dv is not None else None
+    d = _device_digit_bits(cfg)
+    sorter = DeviceSorter(n, dk.dtype, vb, d, begin_bit, end_bit, cfg.tile_size, cfg.strip_size,
+                          device=dk.device)
+    sorter(dk, ok, dv, ov, stream=stream if stream is not None else executor.stream)
+    executor.ledger_record("histogram", "element_reads", n)
+    executor.ledger_record("partition", "element_reads", sorter.passes * n)
+    executor.ledger_record("partition", "element_writes", sorter.passes * n)
+    executor.record_device_stats("partition", sorter.stats, 1 << d)
+    sk = from_device(ok, to_numpy)
+    if values is None:
+        return sk
+    return sk, from_device(ov, to_numpy and not is_tensor(values))
+
+
+def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
+                   executor: Executor | None = None, src_values=None, dst_values=None, *,
+                   return_status: bool = False):
+    """Stable radix-way partition of src into dst by the digit at `place`
+    (binning.py:218-275).
+
+    `offsets` is the place's global bin-offset row or a StripCarry; returns
+    the StripCarry folding in every digit count of this call.  Numpy `dst`
+    arrays are updated in place, as in the reference.  With return_status the
+    final status words are returned as well: a list of per-strip
+    lookback.CounterMatrix views."""
+    import torch
+
+    from .lookback import CounterMatrix
+
+    if cfg.digit_bits > MAX_DEVICE_DIGIT_BITS:
+        raise ValueError(f"device passes bin at most {MAX_DEVICE_DIGIT_BITS} bits per place")
+    executor = executor or Executor()
+    shift = cfg.digit_shift(place)
+    src_np = not is_tensor(src_keys)
+    sk, _ = as_device(src_keys)
+    if sk.element_size() * 8 != cfg.key_bits:
+        raise ValueError(f"config is for {cfg.key_bits}-bit keys")
+    dk, _ = as_device(dst_keys)
+    sv = dv = None
+    vb = _val_bytes(src_values)
+    if src_values is not None:
+        sv, _ = as_device(src_values)
+        dv, _ = as_device(dst_values)
+    base = offsets.offsets if isinstance(offsets, StripCarry) else offsets
+    if is_tensor(base):
+        base_dev = base.to(sk.device).contiguous()
+        carry_numpy = False
+    else:
+        base_dev, _ = as_device(np.ascontiguousarray(np.asarray(base, dtype=np.uint64)))
+        carry_numpy = True
+    carry = torch.empty(cfg.radix, dtype=torch.uint64, device=sk.device)
+    L = _native.load()
+    n = sk.numel()
+    cap = L.os_tile_capacity(cfg.key_bits // 8, vb)
+    tile = min(cfg.tile_size, cap)
+    ws = workspace(L.os_partition_workspace_bytes(n, cfg.digit_bits, tile, cfg.strip_size), sk.device)
+    status = None
+    if return_status:
+        words = L.os_partition_status_words(n, cfg.digit_bits, tile, cfg.strip_size)
+        status = torch.zeros(max(words, 1), dtype=torch.int32, device=sk.device)
+    stats = torch.zeros(3, dtype=torch.int64, device=sk.device)
+    _native.check(
+        L.os_partition_pass(_native.ptr(sk), _native.ptr(dk), _native.ptr(sv), _native.ptr(dv), n,
+                            cfg.key_bits // 8, vb, shift, cfg.digit_bits, _native.ptr(base_dev),
+                            _native.ptr(carry), _native.CODEC_NONE, _native.CODEC_NONE, tile,
+                            cfg.strip_size, _native.ptr(status), _native.ptr(ws), ws.numel(),
+                            _native.ptr(stats), _native.stream_handle(executor.stream)),
+        "partition_pass",
+    )
+    executor.ledger_record("partition", "element_reads", n)
+    executor.ledger_record("partition", "element_writes", n)
+    executor.record_device_stats("partition", stats, cfg.radix)
+    if src_np or not is_tensor(dst_keys):
+        np.copyto(dst_keys, dk.cpu().numpy().view(np.asarray(dst_keys).dtype))
+        if dst_values is not None:
+            np.copyto(dst_values, dv.cpu().numpy().view(np.asarray(dst_values).dtype))
+    else:
+        if dk.data_ptr() != dst_keys.data_ptr():
+            dst_keys.copy_(dk)
+        if dst_values is not None and dv.data_ptr() != dst_values.data_ptr():
+            dst_values.copy_(dv)
+    result = StripCarry(carry.cpu().numpy() if carry_numpy else carry)
+    if not return_status:
+        return result
+    words = status.view(torch.uint32).cpu().numpy() if n else np.zeros(0, np.uint32)
+    views, pos = [], 0
+    for lo in range(0, n, cfg.strip_size):
+        tiles = -(-min(cfg.strip_size, n - lo) // tile)
+        views.append(CounterMatrix(words[pos: pos + tiles * cfg.radix].reshape(tiles, cfg.radix)))
+        pos += tiles * cfg.radix
+    return result, views

@@ -1,0 +1,555 @@
+// extern "C" boundary (include/onesweep_b200.h): argument validation,
+// workspace carving and kernel orchestration.  Mirrors the reference's
+// onesweep_sort / partition_pass / global_histograms control flow
+// (binning.py:218-337, histogram.py:57-99) with device kernels doing all the
+// element work -- there is no host compute path.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/onesweep_b200.h"
+#include "common.cuh"
+
+namespace osb {
+int histogram_grid_size();
+}
+
+using namespace osb;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(OS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define OS_CUDA(call, where)                       \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct KeyType {
+  int bytes;
+  int enc;  // codec applied when loading native keys
+  int dec;  // codec applied when storing native keys
+};
+
+bool key_type_info(int key_type, KeyType* out) {
+  switch (key_type) {
+    case OS_KEY_U32: *out = {4, CODEC_NONE, CODEC_NONE}; return true;
+    case OS_KEY_U64: *out = {8, CODEC_NONE, CODEC_NONE}; return true;
+    case OS_KEY_I32: *out = {4, CODEC_SIGNED, CODEC_SIGNED}; return true;
+    case OS_KEY_I64: *out = {8, CODEC_SIGNED, CODEC_SIGNED}; return true;
+    case OS_KEY_F32: *out = {4, CODEC_FLOAT_ENC, CODEC_FLOAT_DEC}; return true;
+    case OS_KEY_F64: *out = {8, CODEC_FLOAT_ENC, CODEC_FLOAT_DEC}; return true;
+    default: return false;
+  }
+}
+
+bool valid_val_bytes(int vb) { return vb == 0 || vb == 1 || vb == 2 || vb == 4 || vb == 8; }
+
+// Tiling of one pass: strips of <= strip keys (binning.py:241-246), tiles of
+// tile keys inside each strip (the last tile of a strip may be ragged).
+struct Tiling {
+  size_t n = 0;
+  size_t strip = 0;
+  size_t strips = 0;
+  size_t tiles_total = 0;  // sum over strips
+  uint32_t tile = 0;
+  size_t strip_len(size_t s) const {
+    const size_t lo = s * strip;
+    return (n - lo) < strip ? (n - lo) : strip;
+  }
+  size_t strip_tiles(size_t s) const { return (strip_len(s) + tile - 1) / tile; }
+};
+
+Tiling make_tiling(size_t n, uint32_t tile, size_t strip) {
+  Tiling t;
+  t.n = n;
+  t.tile = tile;
+  t.strip = strip;
+  t.strips = n ? (n + strip - 1) / strip : 0;
+  // tiles per full strip, plus the ragged last strip
+  if (t.strips) {
+    const size_t full = t.strips - 1;
+    t.tiles_total = full * ((strip + tile - 1) / tile) + t.strip_tiles(t.strips - 1);
+  }
+  return t;
+}
+
+int resolve_tile(int tile_keys, int key_bytes, int val_bytes, uint32_t* out) {
+  const int cap = binning_tile_capacity(key_bytes, val_bytes);
+  if (cap <= 0) return fail(OS_ERR_ARG, "unsupported key/value width %d/%d", key_bytes, val_bytes);
+  if (tile_keys < 0) return fail(OS_ERR_ARG, "tile_keys must be >= 0, got %d", tile_keys);
+  *out = uint32_t(tile_keys == 0 || tile_keys > cap ? cap : tile_keys);
+  return OS_OK;
+}
+
+int resolve_strip(size_t strip_keys, size_t* out) {
+  if (strip_keys == 0) strip_keys = kMaxStripKeys;
+  if (strip_keys > kMaxStripKeys)
+    return fail(OS_ERR_ARG, "strip_keys must be <= 2^28, got %zu", strip_keys);
+  *out = strip_keys;
+  return OS_OK;
+}
+
+// Workspace of one pass over all strips: status words, tile tickets and the
+// 64-bit carries chained between strips (binning.py:196-198, 262).
+struct PassWs {
+  size_t status_words = 0;
+  size_t off_status = 0, off_counters = 0, off_carry = 0, bytes = 0, zero_bytes = 0;
+};
+
+PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
+  PassWs w;
+  w.status_words = t.tiles_total * size_t(radix);
+  size_t off = 0;
+  w.off_status = off;
+  if (own_status) off = align_up(off + w.status_words * 4);
+  w.off_counters = off;
+  off = align_up(off + (t.strips ? t.strips : 1) * 4);
+  w.zero_bytes = off;  // status + tickets are zeroed per pass
+  w.off_carry = off;
+  off = align_up(off + (t.strips ? t.strips : 1) * size_t(radix) * 8);
+  w.bytes = off;
+  return w;
+}
+
+// One binning pass over every strip (partition_pass, binning.py:218-275).
+int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int kb, int vb,
+             const Tiling& t, int shift, int width, int radix, const uint8_t* digit_map,
+             const unsigned long long* base0, unsigned long long* carry_final, int codec_in,
+             int codec_out, uint32_t* status, unsigned char* ws, const PassWs& w,
+             unsigned long long* stats, cudaStream_t stream) {
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
+  unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
+  size_t tile_base = 0;
+  const unsigned long long* base = base0;
+  for (size_t s = 0; s < t.strips; ++s) {
+    PassParams p{};
+    const size_t lo = s * t.strip;
+    p.src_keys = static_cast<const unsigned char*>(src_k) + lo * kb;
+    p.dst_keys = dst_k;
+    p.src_vals = vb ? static_cast<const unsigned char*>(src_v) + lo * vb : nullptr;
+    p.dst_vals = vb ? dst_v : nullptr;
+    p.strip_n = uint32_t(t.strip_len(s));
+    p.num_tiles = uint32_t(t.strip_tiles(s));
+    p.tile_keys = t.tile;
+    p.shift = shift;
+    p.mask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
+    p.radix = radix;
+    p.codec_in = codec_in;
+    p.codec_out = codec_out;
+    p.base_offsets = base;
+    const bool last = (s + 1 == t.strips);
+    p.carry_out = last ? carry_final : carries + s * size_t(radix);
+    p.status = status + tile_base * size_t(radix);
+    p.tile_counter = counters + s;
+    p.stats = stats;
+    p.digit_map = digit_map;
+    OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
+    base = p.carry_out;
+    tile_base += p.num_tiles;
+  }
+  return OS_OK;
+}
+
+int check_bits(int key_bytes, int digit_bits, int begin_bit, int end_bit) {
+  const int kbits = key_bytes * 8;
+  if (digit_bits < 1 || digit_bits > kMaxDigitBits)
+    return fail(OS_ERR_ARG, "digit_bits must be in [1, %d] on the device path, got %d",
+                kMaxDigitBits, digit_bits);
+  if (begin_bit < 0 || end_bit > kbits || begin_bit >= end_bit)
+    return fail(OS_ERR_ARG, "need 0 <= begin_bit < end_bit <= %d, got [%d, %d)", kbits,
+                begin_bit, end_bit);
+  return OS_OK;
+}
+
+struct SortLayout {
+  int passes = 0, radix = 0;
+  Tiling t;
+  PassWs pw;
+  size_t off_tmp_k = 0, off_tmp_v = 0, off_offsets = 0, off_zero = 0, off_hist = 0,
+         off_done = 0, off_pass = 0, zero_bytes = 0, total = 0;
+};
+
+SortLayout sort_layout(size_t n, int kb, int vb, int digit_bits, int begin_bit, int end_bit,
+                       uint32_t tile, size_t strip) {
+  SortLayout L;
+  L.passes = (end_bit - begin_bit + digit_bits - 1) / digit_bits;
+  L.radix = 1 << digit_bits;
+  L.t = make_tiling(n, tile, strip);
+  L.pw = pass_ws(L.t, L.radix, true);
+  size_t off = 0;
+  L.off_tmp_k = off;
+  off = align_up(off + (L.passes > 1 ? n * kb : 0));
+  L.off_tmp_v = off;
+  off = align_up(off + (L.passes > 1 ? n * vb : 0));
+  L.off_offsets = off;
+  off = align_up(off + size_t(L.passes) * L.radix * 8);
+  // everything from here on is zeroed by one memset per sort
+  L.off_zero = off;
+  L.off_hist = off;
+  off = align_up(off + size_t(L.passes) * L.radix * 8);
+  L.off_done = off;
+  off = align_up(off + 4);
+  L.off_pass = off;
+  off += size_t(L.passes) * L.pw.bytes;
+  L.zero_bytes = off - L.off_zero;
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* os_version(void) { return "onesweep_b200 0.1.0 (sm_100a)"; }
+const char* os_last_error(void) { return g_err; }
+int os_max_digit_bits(void) { return kMaxDigitBits; }
+int os_tile_capacity(int key_bytes, int val_bytes) {
+  return binning_tile_capacity(key_bytes, val_bytes);
+}
+
+int os_encode(const void* in, void* out, size_t n, int key_type, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  OS_CUDA(launch_codec(in, out, n, kt.bytes, kt.enc, static_cast<cudaStream_t>(stream)),
+          "encode");
+  return OS_OK;
+}
+
+int os_decode(const void* in, void* out, size_t n, int key_type, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  OS_CUDA(launch_codec(in, out, n, kt.bytes, kt.dec, static_cast<cudaStream_t>(stream)),
+          "decode");
+  return OS_OK;
+}
+
+int os_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
+              unsigned long long first_index, void* stream) {
+  if (key_bits != 32 && key_bits != 64)
+    return fail(OS_ERR_ARG, "key_bits must be 32 or 64, got %d", key_bits);
+  if (q < 1) return fail(OS_ERR_ARG, "q must be >= 1, got %d", q);
+  OS_CUDA(launch_keygen(out, n, key_bits, q, seed, first_index, static_cast<cudaStream_t>(stream)),
+          "keygen");
+  return OS_OK;
+}
+
+size_t os_histogram_workspace_bytes(void) { return kAlign; }
+
+int os_histogram(const void* keys, size_t n, int key_bytes, int codec, int digit_bits,
+                 int begin_bit, int end_bit, unsigned long long* hist_out,
+                 unsigned long long* offsets_out, void* workspace, size_t workspace_bytes,
+                 void* stream) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
+  if (int rc = check_bits(key_bytes, digit_bits, begin_bit, end_bit)) return rc;
+  if (codec < CODEC_NONE || codec > CODEC_FLOAT_ENC)
+    return fail(OS_ERR_ARG, "histogram codec must be NONE, SIGNED or FLOAT_ENC");
+  if (workspace_bytes < os_histogram_workspace_bytes() || workspace == nullptr)
+    return fail(OS_ERR_WORKSPACE, "histogram workspace too small");
+  const int passes = (end_bit - begin_bit + digit_bits - 1) / digit_bits;
+  const int radix = 1 << digit_bits;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n > size_t(osb::histogram_grid_size()) * (size_t(1) << 31))
+    return fail(OS_ERR_ARG, "n too large for 32-bit per-block histogram portions");
+  OS_CUDA(cudaMemsetAsync(hist_out, 0, size_t(passes) * radix * 8, s), "histogram memset");
+  OS_CUDA(cudaMemsetAsync(workspace, 0, kAlign, s), "histogram memset");
+  HistParams p{};
+  p.keys = keys;
+  p.n = n;
+  p.codec = codec;
+  p.begin_bit = begin_bit;
+  p.digit_bits = digit_bits;
+  p.passes = passes;
+  p.top_bits = end_bit - (begin_bit + (passes - 1) * digit_bits);
+  p.hist = hist_out;
+  p.offsets = offsets_out;
+  p.done_counter = static_cast<unsigned int*>(workspace);
+  if (n == 0) {
+    if (offsets_out) OS_CUDA(cudaMemsetAsync(offsets_out, 0, size_t(passes) * radix * 8, s), "memset");
+    return OS_OK;
+  }
+  OS_CUDA(launch_histogram(p, key_bytes, s), "histogram launch");
+  return OS_OK;
+}
+
+int os_exclusive_scan(const unsigned long long* counts, int rows, int radix,
+                      unsigned long long* offsets_out, void* stream) {
+  if (rows < 0 || radix < 0) return fail(OS_ERR_ARG, "rows/radix must be >= 0");
+  OS_CUDA(launch_exclusive_scan(counts, rows, radix, offsets_out, static_cast<cudaStream_t>(stream)),
+          "exclusive scan");
+  return OS_OK;
+}
+
+size_t os_partition_status_words(size_t n, int digit_width, int tile_keys, size_t strip_keys) {
+  if (tile_keys <= 0 || digit_width < 1 || digit_width > kMaxDigitBits) return 0;
+  size_t strip = strip_keys ? strip_keys : kMaxStripKeys;
+  Tiling t = make_tiling(n, uint32_t(tile_keys), strip);
+  return t.tiles_total << digit_width;
+}
+
+size_t os_partition_workspace_bytes(size_t n, int digit_width, int tile_keys, size_t strip_keys) {
+  if (tile_keys <= 0 || digit_width < 1 || digit_width > kMaxDigitBits) return 0;
+  size_t strip = strip_keys ? strip_keys : kMaxStripKeys;
+  Tiling t = make_tiling(n, uint32_t(tile_keys), strip);
+  return pass_ws(t, 1 << digit_width, true).bytes;
+}
+
+int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals, void* dst_vals,
+                      size_t n, int key_bytes, int val_bytes, int shift, int digit_width,
+                      const unsigned long long* base_offsets, unsigned long long* carry_out,
+                      int codec_in, int codec_out, int tile_keys, size_t strip_keys,
+                      unsigned int* status_out, void* workspace, size_t workspace_bytes,
+                      os_device_stats* stats, void* stream) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if ((val_bytes == 0) != (src_vals == nullptr) || (val_bytes == 0) != (dst_vals == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  if (digit_width < 1 || digit_width > kMaxDigitBits)
+    return fail(OS_ERR_ARG, "digit width must be in [1, %d]", kMaxDigitBits);
+  if (shift < 0 || shift >= key_bytes * 8) return fail(OS_ERR_ARG, "shift out of range");
+  if (codec_in < 0 || codec_in > 3 || codec_out < 0 || codec_out > 3)
+    return fail(OS_ERR_ARG, "bad codec");
+  uint32_t tile;
+  if (int rc = resolve_tile(tile_keys, key_bytes, val_bytes, &tile)) return rc;
+  size_t strip;
+  if (int rc = resolve_strip(strip_keys, &strip)) return rc;
+  const int radix = 1 << digit_width;
+  Tiling t = make_tiling(n, tile, strip);
+  PassWs w = pass_ws(t, radix, true);
+  if (workspace == nullptr || workspace_bytes < w.bytes)
+    return fail(OS_ERR_WORKSPACE, "partition workspace needs %zu bytes, got %zu", w.bytes,
+                workspace_bytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  uint32_t* status = status_out ? status_out : reinterpret_cast<uint32_t*>(ws + w.off_status);
+  if (n == 0) {
+    OS_CUDA(cudaMemcpyAsync(carry_out, base_offsets, size_t(radix) * 8, cudaMemcpyDeviceToDevice, s),
+            "carry copy");
+    return OS_OK;
+  }
+  OS_CUDA(cudaMemsetAsync(ws, 0, w.zero_bytes, s), "partition memset");
+  if (status_out) OS_CUDA(cudaMemsetAsync(status_out, 0, w.status_words * 4, s), "status memset");
+  return run_pass(src_keys, dst_keys, src_vals, dst_vals, key_bytes, val_bytes, t, shift,
+                  digit_width, radix, nullptr, base_offsets, carry_out, codec_in, codec_out, status,
+                  ws, w, reinterpret_cast<unsigned long long*>(stats), s);
+}
+
+size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_bits,
+                               int begin_bit, int end_bit, int tile_keys, size_t strip_keys) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt) || !valid_val_bytes(val_bytes)) return 0;
+  if (check_bits(kt.bytes, digit_bits, begin_bit, end_bit)) return 0;
+  uint32_t tile;
+  size_t strip;
+  if (resolve_tile(tile_keys, kt.bytes, val_bytes, &tile) || resolve_strip(strip_keys, &strip))
+    return 0;
+  return sort_layout(n, kt.bytes, val_bytes, digit_bits, begin_bit, end_bit, tile, strip).total;
+}
+
+static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                     size_t n, int key_type, int val_bytes, int digit_bits, int begin_bit,
+                     int end_bit, int tile_keys, size_t strip_keys, void* workspace,
+                     size_t workspace_bytes, os_device_stats* stats, void** events,
+                     int num_events, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if ((val_bytes == 0) != (vals_in == nullptr) || (val_bytes == 0) != (vals_out == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  if (int rc = check_bits(kt.bytes, digit_bits, begin_bit, end_bit)) return rc;
+  uint32_t tile;
+  if (int rc = resolve_tile(tile_keys, kt.bytes, val_bytes, &tile)) return rc;
+  size_t strip;
+  if (int rc = resolve_strip(strip_keys, &strip)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int kb = kt.bytes, vb = val_bytes;
+
+  if (n <= 1) {  // binning.py:306-309
+    if (n == 1) {
+      OS_CUDA(cudaMemcpyAsync(keys_out, keys_in, kb, cudaMemcpyDeviceToDevice, s), "copy");
+      if (vb) OS_CUDA(cudaMemcpyAsync(vals_out, vals_in, vb, cudaMemcpyDeviceToDevice, s), "copy");
+    }
+    return OS_OK;
+  }
+  SortLayout L = sort_layout(n, kb, vb, digit_bits, begin_bit, end_bit, tile, strip);
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return fail(OS_ERR_WORKSPACE, "sort workspace needs %zu bytes, got %zu", L.total,
+                workspace_bytes);
+  if (keys_out == keys_in && (L.passes % 2) == 1)
+    return fail(OS_ERR_ARG, "in-place sort needs an even pass count");
+  if (n > size_t(osb::histogram_grid_size()) * (size_t(1) << 31))
+    return fail(OS_ERR_ARG, "n too large");
+
+  if (events != nullptr && num_events < L.passes + 2)
+    return fail(OS_ERR_ARG, "need %d events, got %d", L.passes + 2, num_events);
+  auto mark = [&](int i) -> cudaError_t {
+    return events ? cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s) : cudaSuccess;
+  };
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  OS_CUDA(cudaMemsetAsync(ws + L.off_zero, 0, L.zero_bytes, s), "sort memset");
+  OS_CUDA(mark(0), "event");
+
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(ws + L.off_hist);
+  unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.off_offsets);
+  HistParams hp{};
+  hp.keys = keys_in;
+  hp.n = n;
+  hp.codec = kt.enc;
+  hp.begin_bit = begin_bit;
+  hp.digit_bits = digit_bits;
+  hp.passes = L.passes;
+  hp.top_bits = end_bit - (begin_bit + (L.passes - 1) * digit_bits);
+  hp.hist = hist;
+  hp.offsets = offsets;
+  hp.done_counter = reinterpret_cast<unsigned int*>(ws + L.off_done);
+  OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  OS_CUDA(mark(1), "event");
+
+  // Ping-pong so that the last pass lands in the caller's output buffer
+  // (no parity copy, binning.py:327-334 is never needed).
+  void* tmp_k = ws + L.off_tmp_k;
+  void* tmp_v = ws + L.off_tmp_v;
+  const void* src_k = keys_in;
+  const void* src_v = vals_in;
+  for (int k = 0; k < L.passes; ++k) {
+    const bool to_out = ((L.passes - 1 - k) % 2) == 0;
+    void* dst_k = to_out ? keys_out : tmp_k;
+    void* dst_v = to_out ? vals_out : tmp_v;
+    const int shift = begin_bit + k * digit_bits;
+    const int width = (end_bit - shift) < digit_bits ? (end_bit - shift) : digit_bits;
+    unsigned char* pws = ws + L.off_pass + size_t(k) * L.pw.bytes;
+    uint32_t* status = reinterpret_cast<uint32_t*>(pws + L.pw.off_status);
+    unsigned long long* carry_final =
+        reinterpret_cast<unsigned long long*>(pws + L.pw.off_carry) +
+        (L.t.strips - 1) * size_t(L.radix);
+    int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
+                      offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
+                      k == L.passes - 1 ? kt.dec : CODEC_NONE, status, pws, L.pw,
+                      reinterpret_cast<unsigned long long*>(stats), s);
+    if (rc) return rc;
+    OS_CUDA(mark(2 + k), "event");
+    src_k = dst_k;
+    src_v = dst_v;
+  }
+  return OS_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int os_sort(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out, size_t n,
+            int key_type, int val_bytes, int digit_bits, int begin_bit, int end_bit, int tile_keys,
+            size_t strip_keys, void* workspace, size_t workspace_bytes, os_device_stats* stats,
+            void* stream) {
+  return sort_impl(keys_in, keys_out, vals_in, vals_out, n, key_type, val_bytes, digit_bits,
+                   begin_bit, end_bit, tile_keys, strip_keys, workspace, workspace_bytes, stats,
+                   nullptr, 0, stream);
+}
+
+int os_sort_events(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                   size_t n, int key_type, int val_bytes, int digit_bits, int begin_bit,
+                   int end_bit, int tile_keys, size_t strip_keys, void* workspace,
+                   size_t workspace_bytes, os_device_stats* stats, void** events,
+                   int num_events, void* stream) {
+  return sort_impl(keys_in, keys_out, vals_in, vals_out, n, key_type, val_bytes, digit_bits,
+                   begin_bit, end_bit, tile_keys, strip_keys, workspace, workspace_bytes, stats,
+                   events, num_events, stream);
+}
+
+int os_msd_histogram(const void* keys, size_t n, int key_type, int digit_bits, int end_bit,
+                     unsigned long long* hist_out, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (int rc = check_bits(kt.bytes, digit_bits, end_bit - digit_bits, end_bit)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  OS_CUDA(cudaMemsetAsync(hist_out, 0, (size_t(1) << digit_bits) * 8, s), "memset");
+  if (n == 0) return OS_OK;
+  HistParams p{};
+  p.keys = keys;
+  p.n = n;
+  p.codec = kt.enc;
+  p.begin_bit = end_bit - digit_bits;
+  p.digit_bits = digit_bits;
+  p.passes = 1;
+  p.top_bits = digit_bits;
+  p.hist = hist_out;
+  p.offsets = nullptr;
+  p.done_counter = nullptr;
+  OS_CUDA(launch_histogram(p, kt.bytes, s), "msd histogram launch");
+  return OS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void build_digit_map(const unsigned int* bin_lo, int parts, int radix, uint8_t* map) {
+  const int r = threadIdx.x;
+  if (r >= radix) return;
+  int g = 0;
+  while (g + 1 < parts && bin_lo[g + 1] <= unsigned(r)) ++g;
+  map[r] = uint8_t(g);
+}
+}  // namespace
+
+extern "C" {
+
+size_t os_msd_partition_workspace_bytes(size_t n) {
+  // status/tickets/carries for a pass with up to 256 destinations + the map
+  Tiling t = make_tiling(n, uint32_t(binning_tile_capacity(8, 8)), kMaxStripKeys);
+  return align_up(kMaxRadix) + pass_ws(t, kMaxRadix, true).bytes;
+}
+
+int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                     size_t n, int key_type, int val_bytes, int digit_bits, int end_bit,
+                     const unsigned int* bin_lo, int parts,
+                     const unsigned long long* seg_offsets, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if ((val_bytes == 0) != (vals_in == nullptr) || (val_bytes == 0) != (vals_out == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  if (int rc = check_bits(kt.bytes, digit_bits, end_bit - digit_bits, end_bit)) return rc;
+  if (parts < 1 || parts > kMaxRadix) return fail(OS_ERR_ARG, "parts must be in [1, 256]");
+  if (n == 0) return OS_OK;
+  uint32_t tile;
+  if (int rc = resolve_tile(0, kt.bytes, val_bytes, &tile)) return rc;
+  // the workspace bound was computed with the smallest capacity; any tile
+  // geometry of this build needs at most that many tiles
+  Tiling t = make_tiling(n, tile, kMaxStripKeys);
+  PassWs w = pass_ws(t, parts, true);
+  const size_t need = align_up(kMaxRadix) + w.bytes;
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(OS_ERR_WORKSPACE, "msd workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  uint8_t* map = ws;
+  unsigned char* pws = ws + align_up(kMaxRadix);
+  OS_CUDA(cudaMemsetAsync(pws, 0, w.zero_bytes, s), "msd memset");
+  build_digit_map<<<1, kMaxRadix, 0, s>>>(bin_lo, parts, 1 << digit_bits, map);
+  OS_CUDA(cudaGetLastError(), "digit map");
+  unsigned long long* carry_final =
+      reinterpret_cast<unsigned long long*>(pws + w.off_carry) + (t.strips - 1) * size_t(parts);
+  return run_pass(keys_in, keys_out, vals_in, vals_out, kt.bytes, val_bytes, t,
+                  end_bit - digit_bits, digit_bits, parts, map, seg_offsets, carry_final, kt.enc,
+                  kt.dec, reinterpret_cast<uint32_t*>(pws + w.off_status), pws, w, nullptr, s);
+}
+
+}  // extern "C"

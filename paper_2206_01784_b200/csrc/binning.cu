@@ -1,0 +1,374 @@
+// Chained-scan digit-binning pass (one Onesweep partition pass) for sm_100a.
+//
+// Replaces, for one digit place and one strip, the reference's
+//   partition_pass / process_tile      binning.py:162-275
+//   rank_tile_kernel (WLMS)             _kernels.py:31-82
+//   CounterMatrix publish / look-back   lookback.py:127-169
+//   scatter_tile_kernel / slots kernel  _kernels.py:85-128
+//   short-circuit fast path             binning.py:79-85,201-205
+//   StripCarry write by the last tile   binning.py:196-198
+// with one CUDA kernel in which a thread block processes one tile:
+//
+//   1. claim a tile id from an atomic ticket (forward progress for the
+//      chained scan: ids are handed out in block-start order, executor.py:1-8);
+//   2. stage the tile's keys (and values) into shared memory with one TMA bulk
+//      copy each (cp.async.bulk ... mbarrier::complete_tx), values landing
+//      while the keys are ranked;
+//   3. rank keys with a warp-level multisplit: __match_any_sync on the digit
+//      gives the same-digit peer mask, rank = warp running count + popc of
+//      lower peers (the reference's d ballots collapse into one MATCH.ANY);
+//   4. reduce per-warp digit counts to tile counts (thread i owns digit i,
+//      PAPER.md:187), publish L|count, look back over predecessor status
+//      words with relaxed gpu-scope loads, publish G|inclusive;
+//   5. reorder the tile through shared memory into per-digit runs and write
+//      each run with coalesced stores at base + exclusive + (slot - start);
+//      the codec (signed/float decode) is applied on the way out.
+//
+// Keys move once in and once out: 2n element transfers per pass, the
+// reference's ledger identity (binning.py:268-272).
+#include <cstdio>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace osb {
+
+struct NoValue {};
+template <typename V> struct ValTraits {
+  static constexpr bool kHas = true;
+  static constexpr int kBytes = sizeof(V);
+};
+template <> struct ValTraits<NoValue> {
+  static constexpr bool kHas = false;
+  static constexpr int kBytes = 0;
+};
+
+template <int THREADS, int ITEMS, int KB, int VB>
+struct BinningSmem {
+  static constexpr int kTile = THREADS * ITEMS;
+  static constexpr int kWarps = THREADS / 32;
+  static constexpr size_t kKeys = size_t(kTile) * KB;
+  static constexpr size_t kVals = size_t(kTile) * VB;
+  static constexpr size_t kHist = size_t(kWarps) * kMaxRadix * 4;  // per-warp digit counters
+  static constexpr size_t kAdj = kMaxRadix * 8;                    // u64 scatter base per digit
+  static constexpr size_t kLocal = kMaxRadix * 4;                  // tile-local digit starts
+  static constexpr size_t kWsum = 32 * 4;
+  static constexpr size_t kMap = kMaxRadix;
+  static constexpr size_t kBytes = kKeys + kVals + kHist + kAdj + kLocal + kWsum + kMap;
+};
+
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED>
+__global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
+  constexpr bool HAS_V = ValTraits<V>::kHas;
+  using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
+  constexpr int TILE = Smem::kTile;
+  constexpr int WARPS = Smem::kWarps;
+  static_assert(THREADS >= kMaxRadix, "one thread per digit for the look-back");
+  static_assert(THREADS % 32 == 0, "whole warps");
+  using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  K* s_keys = reinterpret_cast<K*>(smem_raw);
+  VS* s_vals = reinterpret_cast<VS*>(smem_raw + Smem::kKeys);
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem_raw + Smem::kKeys + Smem::kVals);
+  unsigned long long* s_adj = reinterpret_cast<unsigned long long*>(
+      smem_raw + Smem::kKeys + Smem::kVals + Smem::kHist);
+  uint32_t* s_local = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_adj) +
+                                                  Smem::kAdj);
+  uint32_t* s_wsum = s_local + kMaxRadix;
+  uint8_t* s_map = reinterpret_cast<uint8_t*>(s_wsum + 32);
+
+  __shared__ uint32_t s_tile;
+  __shared__ int s_fast;
+  __shared__ uint32_t s_reads;
+  __shared__ __align__(8) uint64_t s_bar_k;
+  __shared__ __align__(8) uint64_t s_bar_v;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int radix = P.radix;
+
+  if (tid == 0) {
+    s_tile = atomicAdd(P.tile_counter, 1u);
+    s_fast = -1;
+    s_reads = 0;
+    mbar_init(&s_bar_k, 1);
+    mbar_init(&s_bar_v, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < WARPS * kMaxRadix; i += THREADS) s_whist[i] = 0;
+  if (MAPPED) {
+    for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
+  }
+  __syncthreads();
+
+  const uint32_t tile = s_tile;
+  const uint32_t tile_start = tile * P.tile_keys;
+  const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
+  const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
+  const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
+
+  // ---- 2. TMA bulk stage ----------------------------------------------------
+  const bool tma_k = ((reinterpret_cast<uintptr_t>(gk) & 15u) == 0) &&
+                     (((valid * sizeof(K)) & 15u) == 0);
+  bool tma_v = false;
+  if (HAS_V)
+    tma_v = ((reinterpret_cast<uintptr_t>(gv) & 15u) == 0) && (((valid * sizeof(VS)) & 15u) == 0);
+  if (tid == 0) {
+    if (tma_k) {
+      mbar_arrive_expect_tx(&s_bar_k, valid * sizeof(K));
+      tma_bulk_g2s(s_keys, gk, valid * sizeof(K), &s_bar_k);
+    }
+    if (HAS_V && tma_v) {
+      mbar_arrive_expect_tx(&s_bar_v, valid * sizeof(VS));
+      tma_bulk_g2s(s_vals, gv, valid * sizeof(VS), &s_bar_v);
+    }
+  }
+
+  // Warp-striped ownership: warp w owns tile positions [w*ITEMS*32, (w+1)*ITEMS*32),
+  // item i / lane l is position w*ITEMS*32 + i*32 + l.  Ranking walks items in
+  // that order, so ranks are stable (binning.py:71-76).
+  const uint32_t warp_base = uint32_t(warp) * (ITEMS * 32);
+  K keys[ITEMS];
+  uint32_t ranks[ITEMS];
+  if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t idx = warp_base + i * 32 + lane;
+    K x;
+    if (tma_k)
+      x = s_keys[idx];
+    else
+      x = idx < valid ? gk[idx] : K(0);
+    keys[i] = apply_codec(x, P.codec_in);
+  }
+
+  // ---- 3. warp-level multisplit ranking -------------------------------------
+  // Positions past `valid` (ragged last tile) take the largest digit: they sit
+  // after every real key, so they never perturb a real key's rank, and their
+  // count is removed from the top digit before publishing.
+  {
+    uint32_t* my_hist = s_whist + warp * kMaxRadix;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      uint32_t d = digit_of(keys[i], P.shift, P.mask);
+      if (MAPPED) d = s_map[d];
+      if (idx >= valid) d = uint32_t(radix - 1);
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = my_hist[d];
+      const uint32_t below = __popc(peers & lt);
+      ranks[i] = before + below;
+      __syncwarp();
+      if ((peers >> lane) == 1u) my_hist[d] = before + __popc(peers);  // highest peer writes
+      __syncwarp();
+    }
+  }
+
+  // Values are consumed after the staging barrier; read them now so the smem
+  // buffer can be reused for the reorder.
+  VS vals[HAS_V ? ITEMS : 1];
+  if (HAS_V) {
+    if (tma_v) mbar_wait_parity(&s_bar_v, 0);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (tma_v)
+        vals[i] = s_vals[idx];
+      else
+        vals[i] = idx < valid ? gv[idx] : VS(0);
+    }
+  }
+  __syncthreads();
+
+  // ---- 4a. tile counts, publish L, local digit starts ------------------------
+  uint32_t count = 0;
+  if (tid < radix) {
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
+    if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
+    count = sum;
+    uint32_t* row = P.status + size_t(tile) * radix;
+    st_relaxed_gpu(row + tid, (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    if (count == valid) s_fast = tid;
+  }
+  // block-wide exclusive scan of counts over digits (first 8 warps)
+  uint32_t incl = count;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31 && warp < kMaxRadix / 32) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t local_start = 0;
+  if (tid < radix) {
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+    local_start = wpre + incl - count;
+    s_local[tid] = local_start;
+    // fold the tile-local start into every warp's exclusive offset so the
+    // staging step needs a single shared-memory gather per key
+    uint32_t run = local_start;
+#pragma unroll 8
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = s_whist[w * kMaxRadix + tid];
+      s_whist[w * kMaxRadix + tid] = run;
+      run += c;
+    }
+
+    // ---- 4b. decoupled look-back (lookback.py:144-169) ----------------------
+    uint32_t excl = 0;
+    uint32_t reads = 0;
+    if (tile > 0) {
+      const uint32_t* col = P.status + tid;
+      int j = int(tile) - 1;
+      while (true) {
+        const uint32_t w = ld_relaxed_gpu(col + size_t(j) * radix);
+        ++reads;
+        const uint32_t st = w >> kStatusShift;
+        if (st == 0u) continue;  // predecessor in flight: it will publish
+        excl += w & kValueMask;
+        if (st == 2u) break;
+        --j;
+      }
+      st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
+    }
+    const unsigned long long gbase = P.base_offsets[tid] + excl;
+    s_adj[tid] = gbase - local_start;
+    if (P.carry_out != nullptr && tile == P.num_tiles - 1) P.carry_out[tid] = gbase + count;
+    if (P.stats != nullptr) atomicAdd(&s_reads, reads);
+  }
+  __syncthreads();
+
+  K* out_k = static_cast<K*>(P.dst_keys);
+  VS* out_v = HAS_V ? static_cast<VS*>(P.dst_vals) : nullptr;
+  const int fast = s_fast;
+
+  if (fast >= 0) {
+    // ---- short circuit: homogeneous tile is one contiguous run --------------
+    const unsigned long long base = s_adj[fast];  // local start is 0
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (idx < valid) {
+        out_k[base + idx] = apply_codec(keys[i], P.codec_out);
+        if (HAS_V) out_v[base + idx] = vals[i];
+      }
+    }
+  } else {
+    // ---- 5. local reorder then coalesced run writes --------------------------
+    const uint32_t* my_off = s_whist + warp * kMaxRadix;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (idx < valid) {
+        uint32_t d = digit_of(keys[i], P.shift, P.mask);
+        if (MAPPED) d = s_map[d];
+        const uint32_t slot = my_off[d] + ranks[i];
+        s_keys[slot] = keys[i];
+        if (HAS_V) s_vals[slot] = vals[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t s = tid; s < valid; s += THREADS) {
+      const K x = s_keys[s];
+      uint32_t d = digit_of(x, P.shift, P.mask);
+      if (MAPPED) d = s_map[d];
+      const unsigned long long g = s_adj[d] + s;
+      out_k[g] = apply_codec(x, P.codec_out);
+      if (HAS_V) out_v[g] = s_vals[s];
+    }
+  }
+
+  if (P.stats != nullptr && tid == 0) {
+    if (fast >= 0) atomicAdd(&P.stats[0], 1ull);
+    atomicAdd(&P.stats[1], (unsigned long long)s_reads);
+    atomicAdd(&P.stats[2], 1ull);
+  }
+}
+
+// ---- host side ------------------------------------------------------------------
+
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED>
+static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
+  using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
+  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Smem::kBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (p.num_tiles == 0) return cudaSuccess;
+  kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// Tile geometry per (key, value) width.  THREADS x ITEMS keys per tile; the
+// shared-memory footprint decides how many tiles an SM keeps in flight.
+template <int KB, int VB> struct Geometry;
+template <> struct Geometry<4, 0> { static constexpr int T = 512, I = 16, B = 2; };
+template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
+template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
+template <> struct Geometry<4, 4> { static constexpr int T = 512, I = 16, B = 2; };
+template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 0> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 1> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 2> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 4> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 8> { static constexpr int T = 512, I = 8, B = 2; };
+
+template <typename K, typename V>
+static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
+  constexpr int KB = sizeof(K);
+  constexpr int VB = ValTraits<V>::kBytes;
+  using G = Geometry<KB, VB>;
+  if (p.tile_keys == 0 || p.tile_keys > uint32_t(G::T * G::I)) return cudaErrorInvalidValue;
+  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true>(p, stream);
+  return launch_one<K, V, G::T, G::I, G::B, false>(p, stream);
+}
+
+template <typename K>
+static cudaError_t dispatch_val(const PassParams& p, int val_bytes, cudaStream_t stream) {
+  switch (val_bytes) {
+    case 0: return dispatch_geom<K, NoValue>(p, stream);
+    case 1: return dispatch_geom<K, uint8_t>(p, stream);
+    case 2: return dispatch_geom<K, uint16_t>(p, stream);
+    case 4: return dispatch_geom<K, uint32_t>(p, stream);
+    case 8: return dispatch_geom<K, uint64_t>(p, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_binning_pass(const PassParams& p, int key_bytes, int val_bytes,
+                                cudaStream_t stream) {
+  if (key_bytes == 4) return dispatch_val<uint32_t>(p, val_bytes, stream);
+  if (key_bytes == 8) return dispatch_val<uint64_t>(p, val_bytes, stream);
+  return cudaErrorInvalidValue;
+}
+
+template <int KB>
+static int capacity_for(int val_bytes) {
+  switch (val_bytes) {
+    case 0: return Geometry<KB, 0>::T * Geometry<KB, 0>::I;
+    case 1: return Geometry<KB, 1>::T * Geometry<KB, 1>::I;
+    case 2: return Geometry<KB, 2>::T * Geometry<KB, 2>::I;
+    case 4: return Geometry<KB, 4>::T * Geometry<KB, 4>::I;
+    case 8: return Geometry<KB, 8>::T * Geometry<KB, 8>::I;
+    default: return 0;
+  }
+}
+
+int binning_tile_capacity(int key_bytes, int val_bytes) {
+  if (key_bytes == 4) return capacity_for<4>(val_bytes);
+  if (key_bytes == 8) return capacity_for<8>(val_bytes);
+  return 0;
+}
+
+}  // namespace osb

@@ -1,0 +1,164 @@
+// Device-side helpers shared by the Onesweep kernels (sm_100a).
+//
+// Reference semantics are cited as /root/reference/pkg/src/onesweep/<file>:<line>.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace osb {
+
+// ---- status words (lookback.py:33-60) -------------------------------------
+// bits 31-30: N=0 / L=1 / G=2, bits 29-0: value.
+constexpr uint32_t kStatusShift = 30;
+constexpr uint32_t kValueMask = (1u << 30) - 1u;
+constexpr uint32_t kFlagLocal = 1u << 30;
+constexpr uint32_t kFlagGlobal = 2u << 30;
+
+constexpr int kMaxDigitBits = 8;
+constexpr int kMaxRadix = 1 << kMaxDigitBits;
+// Strip bound keeps every 30-bit status value in range (binning.py:20-23).
+constexpr size_t kMaxStripKeys = size_t(1) << 28;
+
+enum Codec : int { CODEC_NONE = 0, CODEC_SIGNED = 1, CODEC_FLOAT_ENC = 2, CODEC_FLOAT_DEC = 3 };
+
+template <typename K> struct KeyTraits;
+template <> struct KeyTraits<uint32_t> {
+  static constexpr uint32_t kSign = 0x80000000u;
+  static constexpr int kBits = 32;
+};
+template <> struct KeyTraits<uint64_t> {
+  static constexpr uint64_t kSign = 0x8000000000000000ull;
+  static constexpr int kBits = 64;
+};
+
+// keycodec.py:157-181.  `codec` is warp-uniform, so the switch costs a
+// couple of uniform branches per key in an HBM-bound kernel.
+template <typename K>
+__device__ __forceinline__ K apply_codec(K x, int codec) {
+  constexpr K sign = KeyTraits<K>::kSign;
+  switch (codec) {
+    case CODEC_SIGNED: return x ^ sign;
+    case CODEC_FLOAT_ENC: return (x & sign) ? K(~x) : K(x | sign);
+    case CODEC_FLOAT_DEC: return (x & sign) ? K(x ^ sign) : K(~x);
+    default: return x;
+  }
+}
+
+// keycodec.py:228-239 plus the begin-bit offset: (enc >> shift) & mask.
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K x, int shift, uint32_t mask) {
+  return uint32_t(x >> shift) & mask;
+}
+
+// ---- memory-model helpers ------------------------------------------------
+// Status words are shared between CTAs that may run concurrently on other SMs;
+// a relaxed gpu-scope load/store is single-copy atomic for an aligned 32-bit
+// word and bypasses the (incoherent) L1, which is all the protocol needs: the
+// value travels in the same word as its status (lookback.py:9-13).
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier + TMA bulk copy (global -> shared) ---------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t addr = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+// One bulk (non-tensor) TMA copy; bytes % 16 == 0, both addresses 16B aligned.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- launch descriptors ------------------------------------------------------
+struct PassParams {
+  const void* src_keys;  // strip-relative base already applied by the host
+  void* dst_keys;        // global output base (not strip relative)
+  const void* src_vals;
+  void* dst_vals;
+  uint32_t strip_n;      // keys in this strip (<= 2^28)
+  uint32_t num_tiles;    // ceil(strip_n / tile_keys)
+  uint32_t tile_keys;    // logical tile (<= template capacity)
+  int shift;
+  uint32_t mask;         // radix - 1
+  int radix;
+  int codec_in;
+  int codec_out;
+  const unsigned long long* base_offsets;  // [radix]
+  unsigned long long* carry_out;           // [radix] or null
+  uint32_t* status;                        // [num_tiles][radix], zeroed
+  uint32_t* tile_counter;                  // zeroed
+  unsigned long long* stats;               // os_device_stats or null
+  const uint8_t* digit_map;                // [2^map_bits] -> destination, or null
+};
+
+struct HistParams {
+  const void* keys;
+  size_t n;
+  int codec;
+  int begin_bit;
+  int digit_bits;
+  int passes;
+  int top_bits;  // width of the last place
+  unsigned long long* hist;     // [passes][radix] (zeroed by host)
+  unsigned long long* offsets;  // [passes][radix] or null
+  unsigned int* done_counter;   // zeroed
+};
+
+// Host launchers (defined in the .cu files).
+cudaError_t launch_binning_pass(const PassParams& p, int key_bytes, int val_bytes,
+                                cudaStream_t stream);
+int binning_tile_capacity(int key_bytes, int val_bytes);
+cudaError_t launch_histogram(const HistParams& p, int key_bytes, cudaStream_t stream);
+cudaError_t launch_exclusive_scan(const unsigned long long* counts, int rows, int radix,
+                                  unsigned long long* out, cudaStream_t stream);
+cudaError_t launch_codec(const void* in, void* out, size_t n, int key_bytes, int codec,
+                         cudaStream_t stream);
+cudaError_t launch_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
+                          unsigned long long first, cudaStream_t stream);
+cudaError_t launch_top_histogram(const void* keys, size_t n, int key_bytes, int codec, int shift,
+                                 uint32_t mask, unsigned long long* hist, cudaStream_t stream);
+
+}  // namespace osb
