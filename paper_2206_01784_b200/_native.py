@@ -12,7 +12,10 @@ import ctypes
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libonesweep_b200.so")
+LIB_PATH = os.environ.get(
+    "ONESWEEP_B200_LIB",
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libonesweep_b200.so"),
+)
 
 OS_OK = 0
 OS_ERR_ARG = 1

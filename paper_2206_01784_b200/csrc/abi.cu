@@ -151,8 +151,13 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.shift = shift;
     p.mask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
     p.radix = radix;
-    p.codec_in = codec_in;
-    p.codec_out = codec_out;
+    if (kb == 4) {
+      const auto ci = XorCodec<uint32_t>::make(codec_in), co = XorCodec<uint32_t>::make(codec_out);
+      p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+    } else {
+      const auto ci = XorCodec<uint64_t>::make(codec_in), co = XorCodec<uint64_t>::make(codec_out);
+      p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+    }
     p.base_offsets = base;
     const bool last = (s + 1 == t.strips);
     p.carry_out = last ? carry_final : carries + s * size_t(radix);

@@ -57,7 +57,7 @@ struct BinningSmem {
   static constexpr size_t kBytes = kKeys + kVals + kHist + kAdj + kLocal + kWsum + kMap;
 };
 
-template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED>
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
   constexpr bool HAS_V = ValTraits<V>::kHas;
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   constexpr int WARPS = Smem::kWarps;
   static_assert(THREADS >= kMaxRadix, "one thread per digit for the look-back");
   static_assert(THREADS % 32 == 0, "whole warps");
+  static_assert(TILE < 65536, "ranks are packed as u16");
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -88,6 +89,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int radix = P.radix;
+  const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
+  const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
 
   if (tid == 0) {
     s_tile = atomicAdd(P.tile_counter, 1u);
@@ -128,57 +131,58 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // Warp-striped ownership: warp w owns tile positions [w*ITEMS*32, (w+1)*ITEMS*32),
   // item i / lane l is position w*ITEMS*32 + i*32 + l.  Ranking walks items in
-  // that order, so ranks are stable (binning.py:71-76).
+  // that order, so ranks are stable (binning.py:71-76).  Keys stay in the
+  // shared tile buffer while they are ranked (registers hold only the packed
+  // ranks); ragged or misaligned tiles are first copied there by the threads.
   const uint32_t warp_base = uint32_t(warp) * (ITEMS * 32);
-  K keys[ITEMS];
-  uint32_t ranks[ITEMS];
-  if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+  if (!tma_k) {
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t idx = warp_base + i * 32 + lane;
-    K x;
-    if (tma_k)
-      x = s_keys[idx];
-    else
-      x = idx < valid ? gk[idx] : K(0);
-    keys[i] = apply_codec(x, P.codec_in);
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (idx < valid) s_keys[idx] = gk[idx];
+    }
   }
+  if (HAS_V && !tma_v) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (idx < valid) s_vals[idx] = gv[idx];
+    }
+  }
+  if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+
+  auto load_key = [&](uint32_t idx) -> K {
+    const K x = s_keys[idx];
+    return CODED ? cin(x) : x;
+  };
+  auto digit = [&](K x) -> uint32_t {
+    uint32_t d = digit_of(x, P.shift, P.mask);
+    if (MAPPED) d = s_map[d];
+    return d;
+  };
 
   // ---- 3. warp-level multisplit ranking -------------------------------------
   // Positions past `valid` (ragged last tile) take the largest digit: they sit
   // after every real key, so they never perturb a real key's rank, and their
   // count is removed from the top digit before publishing.
+  uint32_t ranks[(ITEMS + 1) / 2];  // two u16 ranks per register
   {
     uint32_t* my_hist = s_whist + warp * kMaxRadix;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
-      uint32_t d = digit_of(keys[i], P.shift, P.mask);
-      if (MAPPED) d = s_map[d];
-      if (idx >= valid) d = uint32_t(radix - 1);
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      uint32_t d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
+      const uint32_t peers = match_peers<kMaxDigitBits>(d);
       const uint32_t before = my_hist[d];
-      const uint32_t below = __popc(peers & lt);
-      ranks[i] = before + below;
+      const uint32_t rank = before + __popc(peers & lt);
+      if (i & 1)
+        ranks[i / 2] |= rank << 16;
+      else
+        ranks[i / 2] = rank;
       __syncwarp();
       if ((peers >> lane) == 1u) my_hist[d] = before + __popc(peers);  // highest peer writes
       __syncwarp();
-    }
-  }
-
-  // Values are consumed after the staging barrier; read them now so the smem
-  // buffer can be reused for the reorder.
-  VS vals[HAS_V ? ITEMS : 1];
-  if (HAS_V) {
-    if (tma_v) mbar_wait_parity(&s_bar_v, 0);
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t idx = warp_base + i * 32 + lane;
-      if (tma_v)
-        vals[i] = s_vals[idx];
-      else
-        vals[i] = idx < valid ? gv[idx] : VS(0);
     }
   }
   __syncthreads();
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
     count = sum;
-    uint32_t* row = P.status + size_t(tile) * radix;
-    st_relaxed_gpu(row + tid, (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
+                   (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
   // block-wide exclusive scan of counts over digits (first 8 warps)
@@ -219,8 +223,42 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       s_whist[w * kMaxRadix + tid] = run;
       run += c;
     }
+  }
+  // pull this thread's keys (and values) into registers; after the barrier
+  // the tile buffers are rewritten in place as per-digit runs
+  K keys[ITEMS];
+  VS vals[HAS_V ? ITEMS : 1];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t idx = warp_base + i * 32 + lane;
+    keys[i] = load_key(idx);
+  }
+  if (HAS_V) {
+    if (tma_v) mbar_wait_parity(&s_bar_v, 0);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
+  }
+  __syncthreads();
+  const int fast = s_fast;
 
-    // ---- 4b. decoupled look-back (lookback.py:144-169) ----------------------
+  // ---- 5a. local reorder into per-digit runs (needs no global offsets, so it
+  // runs before the look-back and gives predecessors time to publish) ---------
+  if (fast < 0) {
+    const uint32_t* my_off = s_whist + warp * kMaxRadix;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = warp_base + i * 32 + lane;
+      if (idx < valid) {
+        const uint32_t rank = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
+        const uint32_t slot = my_off[digit(keys[i])] + rank;
+        s_keys[slot] = keys[i];
+        if (HAS_V) s_vals[slot] = vals[i];
+      }
+    }
+  }
+
+  // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
+  if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0;
     if (tile > 0) {
@@ -246,7 +284,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   K* out_k = static_cast<K*>(P.dst_keys);
   VS* out_v = HAS_V ? static_cast<VS*>(P.dst_vals) : nullptr;
-  const int fast = s_fast;
 
   if (fast >= 0) {
     // ---- short circuit: homogeneous tile is one contiguous run --------------
@@ -255,32 +292,17 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
-        out_k[base + idx] = apply_codec(keys[i], P.codec_out);
+        out_k[base + idx] = CODED ? cout(keys[i]) : keys[i];
         if (HAS_V) out_v[base + idx] = vals[i];
       }
     }
   } else {
-    // ---- 5. local reorder then coalesced run writes --------------------------
-    const uint32_t* my_off = s_whist + warp * kMaxRadix;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t idx = warp_base + i * 32 + lane;
-      if (idx < valid) {
-        uint32_t d = digit_of(keys[i], P.shift, P.mask);
-        if (MAPPED) d = s_map[d];
-        const uint32_t slot = my_off[d] + ranks[i];
-        s_keys[slot] = keys[i];
-        if (HAS_V) s_vals[slot] = vals[i];
-      }
-    }
-    __syncthreads();
+    // ---- 5b. coalesced run writes --------------------------------------------
 #pragma unroll 4
     for (uint32_t s = tid; s < valid; s += THREADS) {
       const K x = s_keys[s];
-      uint32_t d = digit_of(x, P.shift, P.mask);
-      if (MAPPED) d = s_map[d];
-      const unsigned long long g = s_adj[d] + s;
-      out_k[g] = apply_codec(x, P.codec_out);
+      const unsigned long long g = s_adj[digit(x)] + s;
+      out_k[g] = CODED ? cout(x) : x;
       if (HAS_V) out_v[g] = s_vals[s];
     }
   }
@@ -294,10 +316,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
 // ---- host side ------------------------------------------------------------------
 
-template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED>
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
 static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
-  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED>;
+  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -313,7 +335,10 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
 // Tile geometry per (key, value) width.  THREADS x ITEMS keys per tile; the
 // shared-memory footprint decides how many tiles an SM keeps in flight.
 template <int KB, int VB> struct Geometry;
-template <> struct Geometry<4, 0> { static constexpr int T = 512, I = 16, B = 2; };
+#ifndef OS_U32_MINB
+#define OS_U32_MINB 2
+#endif
+template <> struct Geometry<4, 0> { static constexpr int T = 512, I = 16, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 4> { static constexpr int T = 512, I = 16, B = 2; };
@@ -330,8 +355,10 @@ static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
   constexpr int VB = ValTraits<V>::kBytes;
   using G = Geometry<KB, VB>;
   if (p.tile_keys == 0 || p.tile_keys > uint32_t(G::T * G::I)) return cudaErrorInvalidValue;
-  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true>(p, stream);
-  return launch_one<K, V, G::T, G::I, G::B, false>(p, stream);
+  const bool coded = (p.cin_m0 | p.cin_m1 | p.cout_m0 | p.cout_m1) != 0;
+  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true, true>(p, stream);
+  if (coded) return launch_one<K, V, G::T, G::I, G::B, false, true>(p, stream);
+  return launch_one<K, V, G::T, G::I, G::B, false, false>(p, stream);
 }
 
 template <typename K>

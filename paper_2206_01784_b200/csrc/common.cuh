@@ -5,6 +5,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <type_traits>
+
 #include <cuda_runtime.h>
 
 namespace osb {
@@ -33,8 +35,8 @@ template <> struct KeyTraits<uint64_t> {
   static constexpr int kBits = 64;
 };
 
-// keycodec.py:157-181.  `codec` is warp-uniform, so the switch costs a
-// couple of uniform branches per key in an HBM-bound kernel.
+// keycodec.py:157-181.  Scalar form, for host-side planning and the
+// elementwise kernels.
 template <typename K>
 __device__ __forceinline__ K apply_codec(K x, int codec) {
   constexpr K sign = KeyTraits<K>::kSign;
@@ -44,6 +46,53 @@ __device__ __forceinline__ K apply_codec(K x, int codec) {
     case CODEC_FLOAT_DEC: return (x & sign) ? K(x ^ sign) : K(~x);
     default: return x;
   }
+}
+
+// Branch-free codec for the per-key loops: every rule above is
+// x ^ (top bit of x ? m1 : m0) with warp-uniform (m0, m1):
+//   none (0, 0)   signed (sign, sign)   float-enc (sign, ~0)   float-dec (~0, sign).
+// A runtime switch here compiles to a BRX jump table per key.
+template <typename K>
+struct XorCodec {
+  K m0, m1;
+  __host__ __device__ static XorCodec make(int codec) {
+    constexpr K sign = KeyTraits<K>::kSign;
+    constexpr K ones = ~K(0);
+    switch (codec) {
+      case CODEC_SIGNED: return {sign, sign};
+      case CODEC_FLOAT_ENC: return {sign, ones};
+      case CODEC_FLOAT_DEC: return {ones, sign};
+      default: return {K(0), K(0)};
+    }
+  }
+  __device__ __forceinline__ K operator()(K x) const {
+    using S = typename std::conditional<sizeof(K) == 4, int32_t, int64_t>::type;
+    const K top = K(S(x) >> (KeyTraits<K>::kBits - 1));  // all ones iff the top bit is set
+    return x ^ (m0 ^ (top & (m0 ^ m1)));
+  }
+};
+
+// Warp multisplit peer mask for a digit of up to 8 bits, from ballots
+// (one VOTE per digit bit on the ALU pipe; R2P extracts 7 bit-predicates in
+// one instruction).  __match_any_sync computes the same mask but issues on the
+// ADU pipe at ~1 per 16 cycles per SMSP, which capped the first kernel at
+// ~14% of HBM bandwidth (profiles/round1_v1_binning.md).
+template <int BITS>
+__device__ __forceinline__ uint32_t match_peers(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    uint32_t m;
+    asm("{\n\t.reg .pred p;\n\t"
+        "and.b32 %0, %1, %2;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+        "@!p not.b32 %0, %0;\n\t}"
+        : "=r"(m)
+        : "r"(d), "r"(1u << b));
+    peers &= m;
+  }
+  return peers;
 }
 
 // keycodec.py:228-239 plus the begin-bit offset: (enc >> shift) & mask.
@@ -124,8 +173,8 @@ struct PassParams {
   int shift;
   uint32_t mask;         // radix - 1
   int radix;
-  int codec_in;
-  int codec_out;
+  unsigned long long cin_m0, cin_m1;    // XorCodec applied on load
+  unsigned long long cout_m0, cout_m1;  // XorCodec applied on store
   const unsigned long long* base_offsets;  // [radix]
   unsigned long long* carry_out;           // [radix] or null
   uint32_t* status;                        // [num_tiles][radix], zeroed
@@ -137,7 +186,7 @@ struct PassParams {
 struct HistParams {
   const void* keys;
   size_t n;
-  int codec;
+  int codec;  // os_codec applied on load (as a XorCodec)
   int begin_bit;
   int digit_bits;
   int passes;

@@ -3,22 +3,27 @@
 // Replaces global_histograms / histogram_kernel / global_bin_offsets
 // (histogram.py:57-99, _kernels.py:131-145).  One read of every key yields the
 // digit counts of every place (Fig. 5):
-//   - persistent grid (a few blocks per SM), grid-stride over 16-byte vectors;
-//   - per-block shared-memory u32 tables, replicated kCopies times and indexed
-//     by lane % kCopies so same-digit lanes (low-entropy keys) spread over
-//     distinct words instead of serialising on one address;
+//   - persistent grid (one 1024-thread block per SM), grid-stride over
+//     16-byte streaming loads, software-pipelined one batch ahead;
+//   - per-block shared-memory counters with one private copy per LANE, two
+//     u16 counters per u32 word: word = ((place * radix/2 + digit/2) * 32 + lane),
+//     half = digit & 1.  Every shared atomic of a warp therefore hits 32
+//     different banks (one wavefront), whatever the key distribution --
+//     all-equal keys included;
+//   - "portions" (histogram.py:79-88): a lane's u16 counter sees at most
+//     kHistWarps * 16 keys per round, so the block folds its lane copies into
+//     u32 block totals every kRoundsPerPortion rounds, long before 65535;
 //   - one u64 atomicAdd per (place, digit) per block into global memory;
 //   - the last block to finish (atomic ticket) scans each place's row into
 //     exclusive bin offsets, so no separate scan launch is needed.
-// Portions (histogram.py:79-88): a block's share of the input is n / grid keys,
-// so its u32 counters cannot overflow for any n that fits in HBM
-// (grid >= 148 blocks -> n < 148 * 2^32); the host checks the bound.
 #include "common.cuh"
 
 namespace osb {
 
-constexpr int kHistThreads = 512;
-constexpr int kHistCopies = 8;
+constexpr int kHistThreads = 1024;
+constexpr int kHistWarps = kHistThreads / 32;
+constexpr int kHistVec = 4;                       // 16-byte vectors per thread per round
+constexpr int kRoundsPerPortion = 65535 / (kHistWarps * kHistVec * 4);  // u16 headroom
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
   uint4 v;
@@ -30,26 +35,24 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
 
 template <typename K, int FIXED_PASSES>
 struct HistCounter {
-  uint32_t* h;  // this lane's replica base
-  int passes, begin, dbits, radix;
+  uint32_t* lane_base;  // s_hist + lane
+  int passes, begin, dbits, half_radix;
   uint32_t full_mask, top_mask;
-  int codec;
+  XorCodec<K> codec;
 
+  __device__ __forceinline__ void add_place(K x, int p, uint32_t m) const {
+    const uint32_t d = digit_of(x, begin + p * dbits, m);
+    const uint32_t word = (uint32_t(p * half_radix) + (d >> 1)) * 32u;
+    atomicAdd(lane_base + word, 1u << ((d & 1u) << 4));
+  }
   __device__ __forceinline__ void add(K x) const {
-    x = apply_codec(x, codec);
+    x = codec(x);
     if (FIXED_PASSES > 0) {
 #pragma unroll
-      for (int p = 0; p < FIXED_PASSES; ++p) {
-        const uint32_t m = (p == FIXED_PASSES - 1) ? top_mask : full_mask;
-        const uint32_t d = digit_of(x, begin + p * dbits, m);
-        atomicAdd(&h[(p * radix + d) * kHistCopies], 1u);
-      }
+      for (int p = 0; p < FIXED_PASSES; ++p)
+        add_place(x, p, p == FIXED_PASSES - 1 ? top_mask : full_mask);
     } else {
-      for (int p = 0; p < passes; ++p) {
-        const uint32_t m = (p == passes - 1) ? top_mask : full_mask;
-        const uint32_t d = digit_of(x, begin + p * dbits, m);
-        atomicAdd(&h[(p * radix + d) * kHistCopies], 1u);
-      }
+      for (int p = 0; p < passes; ++p) add_place(x, p, p == passes - 1 ? top_mask : full_mask);
     }
   }
   __device__ __forceinline__ void add_vec(uint4 v) const {
@@ -66,28 +69,48 @@ struct HistCounter {
 };
 
 template <typename K, int FIXED_PASSES>
-__global__ void __launch_bounds__(kHistThreads) onesweep_histogram_kernel(const HistParams P) {
-  extern __shared__ uint32_t s_hist[];  // [passes*radix][kHistCopies]
-  __shared__ unsigned long long s_wsum[kHistThreads / 32];
+__global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(const HistParams P) {
+  extern __shared__ uint32_t s_hist[];  // [passes * radix/2][32] lane copies, then u32 totals
+  __shared__ unsigned long long s_wsum[kHistWarps];
   __shared__ bool s_last;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int radix = 1 << P.digit_bits;
+  const int half_radix = radix > 1 ? radix / 2 : 1;
   const int nbins = P.passes * radix;
-  for (int i = tid; i < nbins * kHistCopies; i += kHistThreads) s_hist[i] = 0;
+  const int nwords = P.passes * half_radix * 32;
+  uint32_t* s_total = s_hist + nwords;  // [passes * radix] u32 block totals
+  for (int i = tid; i < nwords + nbins; i += kHistThreads) s_hist[i] = 0;
   __syncthreads();
 
   HistCounter<K, FIXED_PASSES> c;
-  c.h = s_hist + (lane % kHistCopies);
+  c.lane_base = s_hist + lane;
   c.passes = P.passes;
   c.begin = P.begin_bit;
   c.dbits = P.digit_bits;
-  c.radix = radix;
+  c.half_radix = half_radix;
   c.full_mask = uint32_t(radix - 1);
   c.top_mask = uint32_t((1u << P.top_bits) - 1u);
-  c.codec = P.codec;
+  c.codec = XorCodec<K>::make(P.codec);
+
+  // fold the lane copies into the u32 block totals and clear them
+  auto fold = [&]() {
+    __syncthreads();
+    for (int b = tid; b < nbins; b += kHistThreads) {
+      const int p = b / radix, d = b % radix;
+      uint32_t* w = s_hist + (p * half_radix + (d >> 1)) * 32;
+      const int sh = (d & 1) * 16;
+      uint32_t sum = 0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) sum += (w[(l + tid) & 31] >> sh) & 0xffffu;
+      s_total[b] += sum;
+    }
+    __syncthreads();
+    for (int i = tid; i < nwords; i += kHistThreads) s_hist[i] = 0;
+    __syncthreads();
+  };
 
   const K* keys = static_cast<const K*>(P.keys);
   const size_t n = P.n;
@@ -99,31 +122,37 @@ __global__ void __launch_bounds__(kHistThreads) onesweep_histogram_kernel(const 
   const uint4* vp = reinterpret_cast<const uint4*>(keys + head);
 
   const size_t stride = size_t(gridDim.x) * kHistThreads;
-  size_t v = size_t(blockIdx.x) * kHistThreads + tid;
-  for (; v + 3 * stride < nvec; v += 4 * stride) {
-    const uint4 q0 = ld_stream_v4(vp + v);
-    const uint4 q1 = ld_stream_v4(vp + v + stride);
-    const uint4 q2 = ld_stream_v4(vp + v + 2 * stride);
-    const uint4 q3 = ld_stream_v4(vp + v + 3 * stride);
-    c.add_vec(q0);
-    c.add_vec(q1);
-    c.add_vec(q2);
-    c.add_vec(q3);
+  const size_t per_round = stride * kHistVec;
+  const size_t rounds = (nvec + per_round - 1) / per_round;  // same for every block
+  size_t v0 = size_t(blockIdx.x) * kHistThreads + tid;
+
+  uint4 cur[kHistVec];
+#pragma unroll
+  for (int u = 0; u < kHistVec; ++u)
+    if (v0 + u * stride < nvec) cur[u] = ld_stream_v4(vp + v0 + u * stride);
+  for (size_t r = 0; r < rounds; ++r) {
+    const size_t v1 = v0 + per_round;
+    uint4 nxt[kHistVec];
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)  // next batch in flight while this one counts
+      if (v1 + u * stride < nvec) nxt[u] = ld_stream_v4(vp + v1 + u * stride);
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)
+      if (v0 + u * stride < nvec) c.add_vec(cur[u]);
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u) cur[u] = nxt[u];
+    v0 = v1;
+    if ((r + 1) % kRoundsPerPortion == 0) fold();
   }
-  for (; v < nvec; v += stride) c.add_vec(ld_stream_v4(vp + v));
   // unaligned head / ragged tail (< 2 vectors of keys in total)
   const size_t g = size_t(blockIdx.x) * kHistThreads + tid;
   if (g < head) c.add(keys[g]);
   if (tail + g < n) c.add(keys[tail + g]);
-  __syncthreads();
+  fold();
 
-  // flush: reduce replicas, one u64 atomic per non-empty bin
-  for (int i = tid; i < nbins; i += kHistThreads) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int r = 0; r < kHistCopies; ++r) s += s_hist[i * kHistCopies + r];
-    if (s) atomicAdd(&P.hist[i], (unsigned long long)s);
-  }
+  // one u64 atomic per non-empty bin
+  for (int i = tid; i < nbins; i += kHistThreads)
+    if (s_total[i]) atomicAdd(&P.hist[i], (unsigned long long)s_total[i]);
   if (P.offsets == nullptr) return;
 
   // last-block-done: exclusive scan of each place (histogram.py:94-99)
@@ -134,22 +163,20 @@ __global__ void __launch_bounds__(kHistThreads) onesweep_histogram_kernel(const 
   if (!s_last) return;
   __threadfence();
   for (int p = 0; p < P.passes; ++p) {
-    for (int base = 0; base < radix; base += kHistThreads) {
-      const int i = base + tid;
-      const unsigned long long x = (i < radix) ? __ldcg(&P.hist[p * radix + i]) : 0ull;
-      unsigned long long incl = x;
+    const int i = tid;  // radix <= 256 < kHistThreads
+    const unsigned long long x = (i < radix) ? __ldcg(&P.hist[p * radix + i]) : 0ull;
+    unsigned long long incl = x;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      unsigned long long pre = 0;
-      for (int w = 0; w < warp; ++w) pre += s_wsum[w];
-      if (i < radix) P.offsets[p * radix + i] = pre + incl - x;
-      __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
+    if (i < radix) P.offsets[p * radix + i] = pre + incl - x;
+    __syncthreads();
   }
 }
 
@@ -184,13 +211,15 @@ __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const unsigned lon
   }
 }
 
+constexpr size_t kHistMaxSmem = 8 * 128 * 32 * 4 + 8 * 256 * 4 + 4096;
+
 static int hist_grid() {
   static int grid = 0;
   if (grid == 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = sms * 2;
+    grid = sms;
   }
   return grid;
 }
@@ -198,14 +227,17 @@ static int hist_grid() {
 template <typename K, int FIXED>
 static cudaError_t launch_hist_t(const HistParams& p, cudaStream_t stream) {
   auto kern = onesweep_histogram_kernel<K, FIXED>;
-  const size_t smem = size_t(p.passes) * (size_t(1) << p.digit_bits) * kHistCopies * 4;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && configured < smem) {
+  const size_t radix = size_t(1) << p.digit_bits;
+  const size_t half = radix > 1 ? radix / 2 : 1;
+  const size_t smem = (size_t(p.passes) * half * 32 + size_t(p.passes) * radix) * 4;
+  static bool configured = false;
+  if (!configured) {  // largest footprint: 8 places x 256 digits (u64 keys, d = 8) = 136 KiB
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+                                         int(kHistMaxSmem));
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured = true;
   }
+  if (smem > kHistMaxSmem) return cudaErrorInvalidValue;
   kern<<<hist_grid(), kHistThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
