@@ -12,17 +12,17 @@
 //   1. claim a tile id from an atomic ticket (forward progress for the
 //      chained scan: ids are handed out in block-start order, executor.py:1-8);
 //   2. stage the tile's keys (and values) into shared memory with one TMA bulk
-//      copy each (cp.async.bulk ... mbarrier::complete_tx), values landing
-//      while the keys are ranked;
-//   3. rank keys with a warp-level multisplit: __match_any_sync on the digit
-//      gives the same-digit peer mask, rank = warp running count + popc of
-//      lower peers (the reference's d ballots collapse into one MATCH.ANY);
+//      copy each (cp.async.bulk ... mbarrier::complete_tx); values land while
+//      the keys are ranked;
+//   3. rank keys with a warp-level multisplit: eight ballots (one per digit
+//      bit) give the same-digit peer mask, rank = warp running count + popc of
+//      lower peers -- the reference's WLMS (_kernels.py:56-82) on VOTE/LOP3;
 //   4. reduce per-warp digit counts to tile counts (thread i owns digit i,
-//      PAPER.md:187), publish L|count, look back over predecessor status
-//      words with relaxed gpu-scope loads, publish G|inclusive;
-//   5. reorder the tile through shared memory into per-digit runs and write
-//      each run with coalesced stores at base + exclusive + (slot - start);
-//      the codec (signed/float decode) is applied on the way out.
+//      PAPER.md:187), publish L|count, locally reorder the tile into per-digit
+//      runs, then look back over predecessor status words (four in flight per
+//      round trip) and publish G|inclusive;
+//   5. write each run with coalesced stores at base + exclusive + (slot -
+//      start); the codec (signed/float decode) is applied on the way out.
 //
 // Keys move once in and once out: 2n element transfers per pass, the
 // reference's ledger identity (binning.py:268-272).
@@ -48,13 +48,14 @@ struct BinningSmem {
   static constexpr int kTile = THREADS * ITEMS;
   static constexpr int kWarps = THREADS / 32;
   static constexpr size_t kKeys = size_t(kTile) * KB;
-  static constexpr size_t kVals = size_t(kTile) * VB;
+  static constexpr size_t kVals = (size_t(kTile) * VB + 15) / 16 * 16;
   static constexpr size_t kHist = size_t(kWarps) * kMaxRadix * 4;  // per-warp digit counters
-  static constexpr size_t kAdj = kMaxRadix * 8;                    // u64 scatter base per digit
-  static constexpr size_t kLocal = kMaxRadix * 4;                  // tile-local digit starts
+  static constexpr size_t kKPtr = kMaxRadix * 8;  // per-digit output base address (keys)
+  static constexpr size_t kVPtr = VB ? kMaxRadix * 8 : 0;  // (values)
+  static constexpr size_t kLocal = kMaxRadix * 4;  // tile-local digit starts
   static constexpr size_t kWsum = 32 * 4;
   static constexpr size_t kMap = kMaxRadix;
-  static constexpr size_t kBytes = kKeys + kVals + kHist + kAdj + kLocal + kWsum + kMap;
+  static constexpr size_t kBytes = kKeys + kVals + kHist + kKPtr + kVPtr + kLocal + kWsum + kMap;
 };
 
 template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
@@ -66,16 +67,18 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   static_assert(THREADS >= kMaxRadix, "one thread per digit for the look-back");
   static_assert(THREADS % 32 == 0, "whole warps");
   static_assert(TILE < 65536, "ranks are packed as u16");
+  static_assert((WARPS * kMaxRadix) % (4 * THREADS) == 0, "vectorised counter reset");
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   VS* s_vals = reinterpret_cast<VS*>(smem_raw + Smem::kKeys);
   uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem_raw + Smem::kKeys + Smem::kVals);
-  unsigned long long* s_adj = reinterpret_cast<unsigned long long*>(
+  unsigned long long* s_kptr = reinterpret_cast<unsigned long long*>(
       smem_raw + Smem::kKeys + Smem::kVals + Smem::kHist);
-  uint32_t* s_local = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_adj) +
-                                                  Smem::kAdj);
+  unsigned long long* s_vptr = s_kptr + kMaxRadix;  // only when HAS_V
+  uint32_t* s_local = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_kptr) +
+                                                  Smem::kKPtr + Smem::kVPtr);
   uint32_t* s_wsum = s_local + kMaxRadix;
   uint8_t* s_map = reinterpret_cast<uint8_t*>(s_wsum + 32);
 
@@ -89,6 +92,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int radix = P.radix;
+  const int shift = P.shift;
+  const uint32_t dmask = P.mask;
   const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
   const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
 
@@ -100,7 +105,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     mbar_init(&s_bar_v, 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < WARPS * kMaxRadix; i += THREADS) s_whist[i] = 0;
+  {
+    uint4* z = reinterpret_cast<uint4*>(s_whist);
+#pragma unroll
+    for (int i = tid; i < WARPS * kMaxRadix / 4; i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
+  }
   if (MAPPED) {
     for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
   }
@@ -109,6 +118,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const uint32_t tile = s_tile;
   const uint32_t tile_start = tile * P.tile_keys;
   const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
+  const bool full = valid == uint32_t(TILE);
   const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
   const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
 
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     return CODED ? cin(x) : x;
   };
   auto digit = [&](K x) -> uint32_t {
-    uint32_t d = digit_of(x, P.shift, P.mask);
+    uint32_t d = digit_of(x, shift, dmask);
     if (MAPPED) d = s_map[d];
     return d;
   };
@@ -166,32 +176,40 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // after every real key, so they never perturb a real key's rank, and their
   // count is removed from the top digit before publishing.
   uint32_t ranks[(ITEMS + 1) / 2];  // two u16 ranks per register
-  {
+  auto rank_items = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
     uint32_t* my_hist = s_whist + warp * kMaxRadix;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
-      uint32_t d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
-      const uint32_t peers = match_peers<kMaxDigitBits>(d);
-      const uint32_t before = my_hist[d];
-      const uint32_t rank = before + __popc(peers & lt);
+      uint32_t d;
+      if (FULL)
+        d = digit(load_key(idx));
+      else
+        d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
+      const uint32_t peers = match_peers8(d);
+      const uint32_t rank = my_hist[d] + __popc(peers & lt);
       if (i & 1)
-        ranks[i / 2] |= rank << 16;
+        ranks[i / 2] += rank << 16;
       else
         ranks[i / 2] = rank;
       __syncwarp();
-      if ((peers >> lane) == 1u) my_hist[d] = before + __popc(peers);  // highest peer writes
+      if ((peers >> lane) == 1u) my_hist[d] = rank + 1;  // highest peer: count after this batch
       __syncwarp();
     }
-  }
+  };
+  if (full)
+    rank_items(std::true_type{});
+  else
+    rank_items(std::false_type{});
   __syncthreads();
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
   if (tid < radix) {
     uint32_t sum = 0;
-#pragma unroll 8
+#pragma unroll
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
     count = sum;
@@ -215,9 +233,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     local_start = wpre + incl - count;
     s_local[tid] = local_start;
     // fold the tile-local start into every warp's exclusive offset so the
-    // staging step needs a single shared-memory gather per key
+    // reorder needs a single shared-memory gather per key
     uint32_t run = local_start;
-#pragma unroll 8
+#pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const uint32_t c = s_whist[w * kMaxRadix + tid];
       s_whist[w * kMaxRadix + tid] = run;
@@ -229,10 +247,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   K keys[ITEMS];
   VS vals[HAS_V ? ITEMS : 1];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t idx = warp_base + i * 32 + lane;
-    keys[i] = load_key(idx);
-  }
+  for (int i = 0; i < ITEMS; ++i) keys[i] = load_key(warp_base + i * 32 + lane);
   if (HAS_V) {
     if (tma_v) mbar_wait_parity(&s_bar_v, 0);
 #pragma unroll
@@ -245,65 +260,88 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // runs before the look-back and gives predecessors time to publish) ---------
   if (fast < 0) {
     const uint32_t* my_off = s_whist + warp * kMaxRadix;
+    auto stage = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t idx = warp_base + i * 32 + lane;
-      if (idx < valid) {
+      for (int i = 0; i < ITEMS; ++i) {
+        if (!FULL && warp_base + i * 32 + lane >= valid) continue;
         const uint32_t rank = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
         const uint32_t slot = my_off[digit(keys[i])] + rank;
         s_keys[slot] = keys[i];
         if (HAS_V) s_vals[slot] = vals[i];
       }
-    }
+    };
+    if (full)
+      stage(std::true_type{});
+    else
+      stage(std::false_type{});
   }
 
-  // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
+  // ---- 4b. decoupled look-back (lookback.py:144-169), four predecessor words
+  // in flight per round trip; then publish G and the per-digit output bases --
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0;
     if (tile > 0) {
       const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
-      while (true) {
-        const uint32_t w = ld_relaxed_gpu(col + size_t(j) * radix);
-        ++reads;
-        const uint32_t st = w >> kStatusShift;
-        if (st == 0u) continue;  // predecessor in flight: it will publish
-        excl += w & kValueMask;
-        if (st == 2u) break;
-        --j;
+      bool done = false;
+      while (!done) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = (j - k >= 0) ? ld_relaxed_gpu(col + size_t(j - k) * radix) : kFlagGlobal;
+        reads += 4;
+        int k = 0;
+#pragma unroll
+        for (; k < 4; ++k) {
+          const uint32_t st = w[k] >> kStatusShift;
+          if (st == 0u) break;  // predecessor in flight: re-poll from here
+          excl += w[k] & kValueMask;
+          if (st == 2u) {
+            done = true;
+            break;
+          }
+        }
+        j -= k;
       }
       st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
     const unsigned long long gbase = P.base_offsets[tid] + excl;
-    s_adj[tid] = gbase - local_start;
+    const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
+    s_kptr[tid] = reinterpret_cast<unsigned long long>(P.dst_keys) + rel * sizeof(K);
+    if (HAS_V) s_vptr[tid] = reinterpret_cast<unsigned long long>(P.dst_vals) + rel * sizeof(VS);
     if (P.carry_out != nullptr && tile == P.num_tiles - 1) P.carry_out[tid] = gbase + count;
     if (P.stats != nullptr) atomicAdd(&s_reads, reads);
   }
   __syncthreads();
 
-  K* out_k = static_cast<K*>(P.dst_keys);
-  VS* out_v = HAS_V ? static_cast<VS*>(P.dst_vals) : nullptr;
-
   if (fast >= 0) {
     // ---- short circuit: homogeneous tile is one contiguous run --------------
-    const unsigned long long base = s_adj[fast];  // local start is 0
+    K* out_k = reinterpret_cast<K*>(s_kptr[fast]);  // local start is 0
+    VS* out_v = HAS_V ? reinterpret_cast<VS*>(s_vptr[fast]) : nullptr;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
-        out_k[base + idx] = CODED ? cout(keys[i]) : keys[i];
-        if (HAS_V) out_v[base + idx] = vals[i];
+        out_k[idx] = CODED ? cout(keys[i]) : keys[i];
+        if (HAS_V) out_v[idx] = vals[i];
       }
     }
   } else {
-    // ---- 5b. coalesced run writes --------------------------------------------
-#pragma unroll 4
-    for (uint32_t s = tid; s < valid; s += THREADS) {
+    // ---- 5b. coalesced run writes: slot s of digit d lands at kptr[d] + s ----
+    auto write_slot = [&](uint32_t s) {
       const K x = s_keys[s];
-      const unsigned long long g = s_adj[digit(x)] + s;
-      out_k[g] = CODED ? cout(x) : x;
-      if (HAS_V) out_v[g] = s_vals[s];
+      const uint32_t d = digit(x);
+      K* dst = reinterpret_cast<K*>(s_kptr[d]) + s;
+      *dst = CODED ? cout(x) : x;
+      if (HAS_V) reinterpret_cast<VS*>(s_vptr[d])[s] = s_vals[s];
+    };
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) write_slot(uint32_t(j * THREADS + tid));
+    } else {
+      for (uint32_t s = tid; s < valid; s += THREADS) write_slot(s);
     }
   }
 

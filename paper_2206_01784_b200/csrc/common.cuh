@@ -72,27 +72,34 @@ struct XorCodec {
   }
 };
 
-// Warp multisplit peer mask for a digit of up to 8 bits, from ballots
-// (one VOTE per digit bit on the ALU pipe; R2P extracts 7 bit-predicates in
-// one instruction).  __match_any_sync computes the same mask but issues on the
-// ADU pipe at ~1 per 16 cycles per SMSP, which capped the first kernel at
-// ~14% of HBM bandwidth (profiles/round1_v1_binning.md).
-template <int BITS>
-__device__ __forceinline__ uint32_t match_peers(uint32_t d) {
-  uint32_t peers = 0xffffffffu;
-#pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-    uint32_t m;
-    asm("{\n\t.reg .pred p;\n\t"
-        "and.b32 %0, %1, %2;\n\t"
-        "setp.ne.u32 p, %0, 0;\n\t"
-        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
-        "@!p not.b32 %0, %0;\n\t}"
-        : "=r"(m)
-        : "r"(d), "r"(1u << b));
-    peers &= m;
-  }
-  return peers;
+// Warp multisplit peer mask for an 8-bit digit, from ballots: one VOTE per
+// digit bit on the ALU pipe, the complement taken by the lanes whose bit is
+// clear, and the eight masks folded with three-input LOP3s.  __match_any_sync
+// computes the same mask but issues on the ADU pipe, which capped the first
+// kernel at ~14% of HBM bandwidth (profiles/round1_binning_v1.md).
+__device__ __forceinline__ uint32_t vote_bit(uint32_t d, uint32_t bit) {
+  uint32_t m;  // ballot of "bit set", complemented by the lanes whose bit is clear
+  asm("{\n\t.reg .pred p;\n\t"
+      "and.b32 %0, %1, %2;\n\t"
+      "setp.ne.u32 p, %0, 0;\n\t"
+      "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+      "@!p not.b32 %0, %0;\n\t}"
+      : "=r"(m)
+      : "r"(d), "r"(bit));
+  return m;
+}
+__device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// Written as eight separate ballots so ptxas extracts seven bit predicates
+// with one R2P; the masks fold with three-input LOP3s.
+__device__ __forceinline__ uint32_t match_peers8(uint32_t d) {
+  const uint32_t v0 = vote_bit(d, 1), v1 = vote_bit(d, 2), v2 = vote_bit(d, 4),
+                 v3 = vote_bit(d, 8), v4 = vote_bit(d, 16), v5 = vote_bit(d, 32),
+                 v6 = vote_bit(d, 64), v7 = vote_bit(d, 128);
+  return and3(and3(v0, v1, v2), and3(v3, v4, v5), v6 & v7);
 }
 
 // keycodec.py:228-239 plus the begin-bit offset: (enc >> shift) & mask.

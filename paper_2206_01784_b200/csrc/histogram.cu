@@ -180,6 +180,109 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
   }
 }
 
+// Specialisation for the headline shape: 32-bit keys, four byte-aligned
+// 8-bit places (begin_bit 0, end_bit 32).  Counters are lane-private u32
+// (4 places x 256 digits x 32 lanes = 128 KiB, bank = lane: conflict-free and
+// never near overflow), the digit is one PRMT byte extract and the counter
+// address one LEA, so a key costs four (PRMT, LEA, ATOMS) triples.
+constexpr size_t kHistU32Smem = 4 * 256 * 32 * 4;
+
+template <bool CODED>
+__global__ void __launch_bounds__(kHistThreads, 1)
+    onesweep_histogram_u32d8_kernel(const HistParams P) {
+  extern __shared__ uint32_t s_cnt[];  // [place][digit][lane]
+  __shared__ unsigned long long s_wsum[kHistWarps];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  {
+    uint4* z = reinterpret_cast<uint4*>(s_cnt);
+    for (int i = tid; i < int(kHistU32Smem / 16); i += kHistThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const XorCodec<uint32_t> codec = XorCodec<uint32_t>::make(P.codec);
+  const uint32_t lane_base = smem_u32(s_cnt) + uint32_t(lane) * 4u;
+  auto add = [&](uint32_t x) {
+    if (CODED) x = codec(x);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t d = __byte_perm(x, 0u, 0x4440u + p);
+      const uint32_t addr = lane_base + (uint32_t(p) << 15) + (d << 7);
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+    }
+  };
+  auto add_vec = [&](uint4 v) {
+    add(v.x);
+    add(v.y);
+    add(v.z);
+    add(v.w);
+  };
+
+  const uint32_t* keys = static_cast<const uint32_t*>(P.keys);
+  const size_t n = P.n;
+  size_t head = ((16u - (reinterpret_cast<uintptr_t>(keys) & 15u)) & 15u) / 4;
+  if (head > n) head = n;
+  const size_t nvec = (n - head) / 4;
+  const size_t tail = head + nvec * 4;
+  const uint4* vp = reinterpret_cast<const uint4*>(keys + head);
+  const size_t stride = size_t(gridDim.x) * kHistThreads;
+  const size_t per_round = stride * kHistVec;
+  size_t v0 = size_t(blockIdx.x) * kHistThreads + tid;
+  uint4 cur[kHistVec];
+#pragma unroll
+  for (int u = 0; u < kHistVec; ++u)
+    if (v0 + u * stride < nvec) cur[u] = ld_stream_v4(vp + v0 + u * stride);
+  while (v0 < nvec) {
+    const size_t v1 = v0 + per_round;
+    uint4 nxt[kHistVec];
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)  // next batch in flight while this one counts
+      if (v1 + u * stride < nvec) nxt[u] = ld_stream_v4(vp + v1 + u * stride);
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)
+      if (v0 + u * stride < nvec) add_vec(cur[u]);
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u) cur[u] = nxt[u];
+    v0 = v1;
+  }
+  const size_t g = size_t(blockIdx.x) * kHistThreads + tid;
+  if (g < head) add(keys[g]);
+  if (tail + g < n) add(keys[tail + g]);
+  __syncthreads();
+
+  // reduce the 32 lane copies of each bin; one u64 atomic per non-empty bin
+  for (int b = tid; b < 4 * 256; b += kHistThreads) {
+    const uint32_t* w = s_cnt + b * 32;
+    uint32_t s = 0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) s += w[(l + lane) & 31];
+    if (s) atomicAdd(&P.hist[b], (unsigned long long)s);
+  }
+  if (P.offsets == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int p = 0; p < 4; ++p) {
+    const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
+    unsigned long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
+    if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
+    __syncthreads();
+  }
+}
+
 // Standalone per-row exclusive scan (one block per row, any radix).
 __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const unsigned long long* counts,
                                                               int radix,
@@ -242,11 +345,28 @@ static cudaError_t launch_hist_t(const HistParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <bool CODED>
+static cudaError_t launch_hist_u32d8(const HistParams& p, cudaStream_t stream) {
+  auto kern = onesweep_histogram_u32d8_kernel<CODED>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kHistU32Smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<hist_grid(), kHistThreads, kHistU32Smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_histogram(const HistParams& p, int key_bytes, cudaStream_t stream) {
   if (p.n == 0) return cudaSuccess;
   const bool full8 = p.digit_bits == 8 && p.top_bits == 8;
   if (key_bytes == 4) {
-    if (full8 && p.passes == 4) return launch_hist_t<uint32_t, 4>(p, stream);
+    if (full8 && p.passes == 4 && p.begin_bit == 0) {
+      if (p.codec != CODEC_NONE) return launch_hist_u32d8<true>(p, stream);
+      return launch_hist_u32d8<false>(p, stream);
+    }
     return launch_hist_t<uint32_t, 0>(p, stream);
   }
   if (key_bytes == 8) {
