@@ -122,6 +122,20 @@ __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Stores through addresses rebuilt from integers: keep them STG (global),
+// not generic ST.
+template <typename T>
+__device__ __forceinline__ void st_global(T* p, T v) {
+  if constexpr (sizeof(T) == 8)
+    asm volatile("st.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");
+  else if constexpr (sizeof(T) == 4)
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"((uint32_t)v) : "memory");
+  else if constexpr (sizeof(T) == 2)
+    asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+  else
+    asm volatile("st.global.b8 [%0], %1;" ::"l"(p), "r"((uint32_t)v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
