@@ -19,8 +19,8 @@
 //      lower peers -- the reference's WLMS (_kernels.py:56-82) on VOTE/LOP3;
 //   4. reduce per-warp digit counts to tile counts (thread i owns digit i,
 //      PAPER.md:187), publish L|count, locally reorder the tile into per-digit
-//      runs, then look back over predecessor status words (four in flight per
-//      round trip) and publish G|inclusive;
+//      runs, then look back over predecessor status words (a window of
+//      predecessors per round trip) and publish G|inclusive;
 //   5. write each run with coalesced stores at base + exclusive + (slot -
 //      start); the codec (signed/float decode) is applied on the way out.
 //
@@ -42,6 +42,11 @@ template <> struct ValTraits<NoValue> {
   static constexpr bool kHas = false;
   static constexpr int kBytes = 0;
 };
+
+#ifndef OS_LOOKBACK_WINDOW
+#define OS_LOOKBACK_WINDOW 16
+#endif
+constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 
 template <int THREADS, int ITEMS, int KB, int VB>
 struct BinningSmem {
@@ -171,17 +176,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     return d;
   };
 
-  // ---- 3. early counts: per-warp digit histogram, then publish L ----------
-  // Counting first (one shared atomic per key) lets the tile publish its
-  // L words before the expensive ranking, so successors' look-backs rarely
-  // find a not-ready predecessor, and it seeds the ranking counters with each
-  // warp's final offsets so a rank is directly the key's slot in the tile.
+  // ---- 3. warp-level multisplit ranking -------------------------------------
   // Positions past `valid` (ragged last tile) take the largest digit: they sit
   // after every real key, so they never perturb a real key's rank, and their
   // count is removed from the top digit before publishing.
-  uint32_t* my_hist = s_whist + warp * kMaxRadix;
-  auto count_items = [&](auto full_tag) {
+  uint32_t ranks[(ITEMS + 1) / 2];  // two u16 ranks per register
+  auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
+    uint32_t* my_hist = s_whist + warp * kMaxRadix;
+    const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
@@ -190,15 +193,24 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         d = digit(load_key(idx));
       else
         d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
-      atomicAdd(my_hist + d, 1u);
+      const uint32_t peers = match_peers8(d);
+      const uint32_t rank = my_hist[d] + __popc(peers & lt);
+      if (i & 1)
+        ranks[i / 2] += rank << 16;
+      else
+        ranks[i / 2] = rank;
+      __syncwarp();
+      if ((peers >> lane) == 1u) my_hist[d] = rank + 1;  // highest peer: count after this batch
+      __syncwarp();
     }
   };
   if (full)
-    count_items(std::true_type{});
+    rank_items(std::true_type{});
   else
-    count_items(std::false_type{});
+    rank_items(std::false_type{});
   __syncthreads();
 
+  // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
   if (tid < radix) {
     uint32_t sum = 0;
@@ -225,7 +237,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
     local_start = wpre + incl - count;
     s_local[tid] = local_start;
-    // seed each warp's counter with its exclusive offset in the tile
+    // fold the tile-local start into every warp's exclusive offset so the
+    // reorder needs a single shared-memory gather per key
     uint32_t run = local_start;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
@@ -234,49 +247,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       run += c;
     }
   }
-  // first look-back window in flight while the tile is ranked
-  uint32_t lb[4];
-  const uint32_t* lb_col = P.status + tid;
-  if (tid < radix && tile > 0) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      lb[k] = (int(tile) - 1 - k >= 0) ? ld_relaxed_gpu(lb_col + size_t(tile - 1 - k) * radix)
-                                        : kFlagGlobal;
-  }
-  __syncthreads();
-  const int fast = s_fast;
-
-  // ---- 4. warp-level multisplit ranking: slot = seeded counter + lower peers
-  uint32_t slots[(ITEMS + 1) / 2];  // two u16 slots per register
-  if (fast < 0) {
-    auto rank_items = [&](auto full_tag) {
-      constexpr bool FULL = decltype(full_tag)::value;
-      const uint32_t lt = lanemask_lt();
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const uint32_t idx = warp_base + i * 32 + lane;
-        uint32_t d;
-        if (FULL)
-          d = digit(load_key(idx));
-        else
-          d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
-        const uint32_t peers = match_peers8(d);
-        const uint32_t slot = my_hist[d] + __popc(peers & lt);
-        if (i & 1)
-          slots[i / 2] += slot << 16;
-        else
-          slots[i / 2] = slot;
-        __syncwarp();
-        if ((peers >> lane) == 1u) my_hist[d] = slot + 1;  // highest peer advances the run
-        __syncwarp();
-      }
-    };
-    if (full)
-      rank_items(std::true_type{});
-    else
-      rank_items(std::false_type{});
-  }
-
   // pull this thread's keys (and values) into registers; after the barrier
   // the tile buffers are rewritten in place as per-digit runs
   K keys[ITEMS];
@@ -289,15 +259,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
   }
   __syncthreads();
+  const int fast = s_fast;
 
-  // ---- 5a. local reorder into per-digit runs ---------------------------------
+  // ---- 5a. local reorder into per-digit runs (needs no global offsets, so it
+  // runs before the look-back and gives predecessors time to publish) ---------
   if (fast < 0) {
+    const uint32_t* my_off = s_whist + warp * kMaxRadix;
     auto stage = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
-        const uint32_t slot = (i & 1) ? (slots[i / 2] >> 16) : (slots[i / 2] & 0xffffu);
+        const uint32_t rank = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
+        const uint32_t slot = my_off[digit(keys[i])] + rank;
         s_keys[slot] = keys[i];
         if (HAS_V) s_vals[slot] = vals[i];
       }
@@ -308,33 +282,37 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       stage(std::false_type{});
   }
 
-  // ---- 4b. decoupled look-back (lookback.py:144-169), four predecessor words
-  // per round trip (the first window was issued before ranking); then publish
-  // G and the per-digit output bases -----------------------------------------
+  // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
+  // A new tile starts every ~30 ns while a status round trip through L2 takes
+  // ~0.5-1 us, so the most recent G is typically 15-30 tiles back: each round
+  // trip therefore reads kLookbackWindow predecessor words at once (one
+  // look-back instead of several when the window was 4).  Then publish G and
+  // the per-digit output bases.
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0;
     if (tile > 0) {
+      const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
       bool done = false;
-      while (true) {
-        reads += 4;
+      while (!done) {
+        uint32_t w[kLookbackWindow];
+#pragma unroll
+        for (int k = 0; k < kLookbackWindow; ++k)
+          w[k] = (j - k >= 0) ? ld_relaxed_gpu(col + size_t(j - k) * radix) : kFlagGlobal;
+        reads += kLookbackWindow;
         int k = 0;
 #pragma unroll
-        for (; k < 4; ++k) {
-          const uint32_t st = lb[k] >> kStatusShift;
+        for (; k < kLookbackWindow; ++k) {
+          const uint32_t st = w[k] >> kStatusShift;
           if (st == 0u) break;  // predecessor in flight: re-poll from here
-          excl += lb[k] & kValueMask;
+          excl += w[k] & kValueMask;
           if (st == 2u) {
             done = true;
             break;
           }
         }
-        if (done) break;
         j -= k;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          lb[q] = (j - q >= 0) ? ld_relaxed_gpu(lb_col + size_t(j - q) * radix) : kFlagGlobal;
       }
       st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
