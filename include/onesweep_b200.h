@@ -64,6 +64,8 @@ typedef struct os_device_stats {
   unsigned long long fast_path_tiles; /* short-circuit tiles (binning.py:201-205) */
   unsigned long long lookback_reads;  /* status words read in look-back (lookback.py:144-169) */
   unsigned long long tiles;           /* tiles processed */
+  unsigned long long lookback_waits;  /* look-back rounds that met a not-ready (N) word */
+  unsigned long long lookback_rounds; /* look-back round trips */
 } os_device_stats;
 
 const char* os_version(void);

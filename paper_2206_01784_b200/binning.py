@@ -140,7 +140,7 @@ class DeviceSorter:
             raise ValueError("invalid sort parameters: " + L.os_last_error().decode())
         self.device = torch.device(device or "cuda")
         self.ws = workspace(nbytes, self.device)
-        self.stats = torch.zeros(3, dtype=torch.int64, device=self.device)
+        self.stats = torch.zeros(5, dtype=torch.int64, device=self.device)
 
     def __call__(self, keys, keys_out, values=None, values_out=None, stream=None, stats=True):
         _native.check(
@@ -255,7 +255,7 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
     if return_status:
         words = L.os_partition_status_words(n, cfg.digit_bits, tile, cfg.strip_size)
         status = torch.zeros(max(words, 1), dtype=torch.int32, device=sk.device)
-    stats = torch.zeros(3, dtype=torch.int64, device=sk.device)
+    stats = torch.zeros(5, dtype=torch.int64, device=sk.device)
     _native.check(
         L.os_partition_pass(_native.ptr(sk), _native.ptr(dk), _native.ptr(sv), _native.ptr(dv), n,
                             cfg.key_bits // 8, vb, shift, cfg.digit_bits, _native.ptr(base_dev),

@@ -74,6 +74,15 @@ struct Tiling {
     return (n - lo) < strip ? (n - lo) : strip;
   }
   size_t strip_tiles(size_t s) const { return (strip_len(s) + tile - 1) / tile; }
+  // look-back granules: clusters of kClusterTiles consecutive tiles
+  size_t strip_supers(size_t s) const {
+    return (strip_tiles(s) + kClusterTiles - 1) / kClusterTiles;
+  }
+  size_t supers_total() const {
+    size_t t = 0;
+    for (size_t s = 0; s < strips; ++s) t += strip_supers(s);
+    return t;
+  }
 };
 
 Tiling make_tiling(size_t n, uint32_t tile, size_t strip) {
@@ -106,8 +115,9 @@ int resolve_strip(size_t strip_keys, size_t* out) {
   return OS_OK;
 }
 
-// Workspace of one pass over all strips: status words, tile tickets and the
-// 64-bit carries chained between strips (binning.py:196-198, 262).
+// Workspace of one pass over all strips: look-back status words (one row per
+// super-tile), tile tickets and the 64-bit carries chained between strips
+// (binning.py:196-198, 262).
 struct PassWs {
   size_t status_words = 0;
   size_t off_status = 0, off_counters = 0, off_carry = 0, bytes = 0, zero_bytes = 0;
@@ -115,7 +125,7 @@ struct PassWs {
 
 PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
   PassWs w;
-  w.status_words = t.tiles_total * size_t(radix);
+  w.status_words = t.supers_total() * size_t(radix);
   size_t off = 0;
   w.off_status = off;
   if (own_status) off = align_up(off + w.status_words * 4);
@@ -132,11 +142,11 @@ PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
 int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int kb, int vb,
              const Tiling& t, int shift, int width, int radix, const uint8_t* digit_map,
              const unsigned long long* base0, unsigned long long* carry_final, int codec_in,
-             int codec_out, uint32_t* status, unsigned char* ws, const PassWs& w,
-             unsigned long long* stats, cudaStream_t stream) {
+             int codec_out, uint32_t* status, uint32_t* tile_status, unsigned char* ws,
+             const PassWs& w, unsigned long long* stats, cudaStream_t stream) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
   unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
-  size_t tile_base = 0;
+  size_t tile_base = 0, super_base = 0;
   const unsigned long long* base = base0;
   for (size_t s = 0; s < t.strips; ++s) {
     PassParams p{};
@@ -161,13 +171,15 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.base_offsets = base;
     const bool last = (s + 1 == t.strips);
     p.carry_out = last ? carry_final : carries + s * size_t(radix);
-    p.status = status + tile_base * size_t(radix);
+    p.status = status + super_base * size_t(radix);
+    p.tile_status = tile_status ? tile_status + tile_base * size_t(radix) : nullptr;
     p.tile_counter = counters + s;
     p.stats = stats;
     p.digit_map = digit_map;
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
     tile_base += p.num_tiles;
+    super_base += t.strip_supers(s);
   }
   return OS_OK;
 }
@@ -342,17 +354,18 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
                 workspace_bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  uint32_t* status = status_out ? status_out : reinterpret_cast<uint32_t*>(ws + w.off_status);
+  uint32_t* status = reinterpret_cast<uint32_t*>(ws + w.off_status);
   if (n == 0) {
     OS_CUDA(cudaMemcpyAsync(carry_out, base_offsets, size_t(radix) * 8, cudaMemcpyDeviceToDevice, s),
             "carry copy");
     return OS_OK;
   }
   OS_CUDA(cudaMemsetAsync(ws, 0, w.zero_bytes, s), "partition memset");
-  if (status_out) OS_CUDA(cudaMemsetAsync(status_out, 0, w.status_words * 4, s), "status memset");
+  if (status_out)
+    OS_CUDA(cudaMemsetAsync(status_out, 0, t.tiles_total * size_t(radix) * 4, s), "status memset");
   return run_pass(src_keys, dst_keys, src_vals, dst_vals, key_bytes, val_bytes, t, shift,
                   digit_width, radix, nullptr, base_offsets, carry_out, codec_in, codec_out, status,
-                  ws, w, reinterpret_cast<unsigned long long*>(stats), s);
+                  status_out, ws, w, reinterpret_cast<unsigned long long*>(stats), s);
 }
 
 size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_bits,
@@ -445,7 +458,7 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
         (L.t.strips - 1) * size_t(L.radix);
     int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
                       offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
-                      k == L.passes - 1 ? kt.dec : CODEC_NONE, status, pws, L.pw,
+                      k == L.passes - 1 ? kt.dec : CODEC_NONE, status, nullptr, pws, L.pw,
                       reinterpret_cast<unsigned long long*>(stats), s);
     if (rc) return rc;
     OS_CUDA(mark(2 + k), "event");
@@ -554,7 +567,8 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in, v
       reinterpret_cast<unsigned long long*>(pws + w.off_carry) + (t.strips - 1) * size_t(parts);
   return run_pass(keys_in, keys_out, vals_in, vals_out, kt.bytes, val_bytes, t,
                   end_bit - digit_bits, digit_bits, parts, map, seg_offsets, carry_final, kt.enc,
-                  kt.dec, reinterpret_cast<uint32_t*>(pws + w.off_status), pws, w, nullptr, s);
+                  kt.dec, reinterpret_cast<uint32_t*>(pws + w.off_status), nullptr, pws, w, nullptr,
+                  s);
 }
 
 }  // extern "C"

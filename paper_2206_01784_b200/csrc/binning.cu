@@ -7,22 +7,31 @@
 //   scatter_tile_kernel / slots kernel  _kernels.py:85-128
 //   short-circuit fast path             binning.py:79-85,201-205
 //   StripCarry write by the last tile   binning.py:196-198
-// with one CUDA kernel in which a thread block processes one tile:
 //
-//   1. claim a tile id from an atomic ticket (forward progress for the
-//      chained scan: ids are handed out in block-start order, executor.py:1-8);
-//   2. stage the tile's keys (and values) into shared memory with one TMA bulk
-//      copy each (cp.async.bulk ... mbarrier::complete_tx); values land while
-//      the keys are ranked;
-//   3. rank keys with a warp-level multisplit: eight ballots (one per digit
+// One CTA bins one tile; a thread-block CLUSTER of CL CTAs bins CL consecutive
+// tiles (a "super-tile") and runs ONE decoupled look-back for all of them:
+//
+//   1. the cluster leader claims a super-tile id from an atomic ticket
+//      (forward progress for the chained scan: ids follow cluster start
+//      order, executor.py:1-8) and the CTAs read it over DSMEM;
+//   2. each CTA stages its tile's keys (and values) into shared memory with
+//      one TMA bulk copy each (cp.async.bulk ... mbarrier::complete_tx);
+//   3. ranks keys with a warp-level multisplit: eight ballots (one per digit
 //      bit) give the same-digit peer mask, rank = warp running count + popc of
 //      lower peers -- the reference's WLMS (_kernels.py:56-82) on VOTE/LOP3;
-//   4. reduce per-warp digit counts to tile counts (thread i owns digit i,
-//      PAPER.md:187), publish L|count, locally reorder the tile into per-digit
-//      runs, then look back over predecessor status words (a window of
-//      predecessors per round trip) and publish G|inclusive;
-//   5. write each run with coalesced stores at base + exclusive + (slot -
-//      start); the codec (signed/float decode) is applied on the way out.
+//   4. reduces per-warp counts to tile counts (thread i owns digit i,
+//      PAPER.md:187) and reorders the tile locally into per-digit runs; the
+//      leader sums the CL tiles' counts over DSMEM, publishes L for the
+//      super-tile, looks back over predecessor super-tiles, publishes G, and
+//      writes each CTA's per-digit global bases into that CTA's shared memory;
+//   5. each CTA writes its runs with coalesced stores at base + (slot - start);
+//      the codec (signed/float decode) is applied on the way out.
+//
+// Why clusters: a tile can publish G only one L2 round trip after the G it
+// found, so the chain advances ~window tiles per round trip; at B200 rates
+// (a tile every ~25 ns) one look-back per 8K-key tile made that chain the
+// limiter.  Per super-tile the chain is CL times shorter and its status
+// traffic CL times smaller (profiles/round1_binning_notes.md).
 //
 // Keys move once in and once out: 2n element transfers per pass, the
 // reference's ledger identity (binning.py:268-272).
@@ -44,7 +53,7 @@ template <> struct ValTraits<NoValue> {
 };
 
 #ifndef OS_LOOKBACK_WINDOW
-#define OS_LOOKBACK_WINDOW 16
+#define OS_LOOKBACK_WINDOW 4
 #endif
 constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 
@@ -57,13 +66,17 @@ struct BinningSmem {
   static constexpr size_t kHist = size_t(kWarps) * kMaxRadix * 4;  // per-warp digit counters
   static constexpr size_t kKPtr = kMaxRadix * 8;  // per-digit output base address (keys)
   static constexpr size_t kVPtr = VB ? kMaxRadix * 8 : 0;  // (values)
+  static constexpr size_t kGBase = kMaxRadix * 8;  // per-digit global base (from the leader)
+  static constexpr size_t kCount = kMaxRadix * 4;  // this tile's digit counts (read by the leader)
   static constexpr size_t kLocal = kMaxRadix * 4;  // tile-local digit starts
   static constexpr size_t kWsum = 32 * 4;
   static constexpr size_t kMap = kMaxRadix;
-  static constexpr size_t kBytes = kKeys + kVals + kHist + kKPtr + kVPtr + kLocal + kWsum + kMap;
+  static constexpr size_t kBytes =
+      kKeys + kVals + kHist + kKPtr + kVPtr + kGBase + kCount + kLocal + kWsum + kMap;
 };
 
-template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
+          int CL>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
   constexpr bool HAS_V = ValTraits<V>::kHas;
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
@@ -72,24 +85,35 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   static_assert(THREADS >= kMaxRadix, "one thread per digit for the look-back");
   static_assert(THREADS % 32 == 0, "whole warps");
   static_assert(TILE < 65536, "ranks are packed as u16");
+  static_assert(size_t(CL) * TILE < (size_t(1) << 30), "super-tile counts fit 30 bits");
   static_assert((WARPS * kMaxRadix) % (4 * THREADS) == 0, "vectorised counter reset");
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  K* s_keys = reinterpret_cast<K*>(smem_raw);
-  VS* s_vals = reinterpret_cast<VS*>(smem_raw + Smem::kKeys);
-  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem_raw + Smem::kKeys + Smem::kVals);
-  unsigned long long* s_kptr = reinterpret_cast<unsigned long long*>(
-      smem_raw + Smem::kKeys + Smem::kVals + Smem::kHist);
-  unsigned long long* s_vptr = s_kptr + kMaxRadix;  // only when HAS_V
-  uint32_t* s_local = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_kptr) +
-                                                  Smem::kKPtr + Smem::kVPtr);
-  uint32_t* s_wsum = s_local + kMaxRadix;
-  uint8_t* s_map = reinterpret_cast<uint8_t*>(s_wsum + 32);
+  unsigned char* sp = smem_raw;
+  K* s_keys = reinterpret_cast<K*>(sp);
+  sp += Smem::kKeys;
+  VS* s_vals = reinterpret_cast<VS*>(sp);
+  sp += Smem::kVals;
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(sp);
+  sp += Smem::kHist;
+  unsigned long long* s_kptr = reinterpret_cast<unsigned long long*>(sp);
+  sp += Smem::kKPtr;
+  unsigned long long* s_vptr = reinterpret_cast<unsigned long long*>(sp);  // only when HAS_V
+  sp += Smem::kVPtr;
+  unsigned long long* s_gbase = reinterpret_cast<unsigned long long*>(sp);
+  sp += Smem::kGBase;
+  uint32_t* s_count = reinterpret_cast<uint32_t*>(sp);
+  sp += Smem::kCount;
+  uint32_t* s_local = reinterpret_cast<uint32_t*>(sp);
+  sp += Smem::kLocal;
+  uint32_t* s_wsum = reinterpret_cast<uint32_t*>(sp);
+  sp += Smem::kWsum;
+  uint8_t* s_map = reinterpret_cast<uint8_t*>(sp);
 
-  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_super;
   __shared__ int s_fast;
-  __shared__ uint32_t s_reads;
+  __shared__ uint32_t s_reads, s_waits, s_rounds;
   __shared__ __align__(8) uint64_t s_bar_k;
   __shared__ __align__(8) uint64_t s_bar_v;
 
@@ -102,10 +126,32 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
   const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
 
+  uint32_t crank = 0;
+  if constexpr (CL > 1) crank = cluster_ctarank();
+  auto cluster_sync = [&]() {
+    if constexpr (CL > 1)
+      cluster_barrier();
+    else
+      __syncthreads();
+  };
+  // DSMEM: read / write CTA r's copy of a shared variable
+  auto remote_ld = [&](const uint32_t* p, uint32_t r) -> uint32_t {
+    if constexpr (CL > 1)
+      return ld_dsmem_u32(dsmem_addr(p, r));
+    else
+      return *p;
+  };
+  auto remote_st = [&](unsigned long long* p, uint32_t r, unsigned long long v) {
+    if constexpr (CL > 1)
+      st_dsmem_u64(dsmem_addr(p, r), v);
+    else
+      *p = v;
+  };
+
   if (tid == 0) {
-    s_tile = atomicAdd(P.tile_counter, 1u);
+    if (crank == 0) s_super = atomicAdd(P.tile_counter, 1u);
     s_fast = -1;
-    s_reads = 0;
+    s_reads = s_waits = s_rounds = 0;
     mbar_init(&s_bar_k, 1);
     mbar_init(&s_bar_v, 1);
     fence_mbar_init();
@@ -118,21 +164,33 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (MAPPED) {
     for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
   }
-  __syncthreads();
+  cluster_sync();
 
-  const uint32_t tile = s_tile;
+  // Non-leaders copy the leader's ticket into their own shared memory first:
+  // feeding a DSMEM load straight into the uniform datapath made ptxas 12.9
+  // fail uniform-predicate allocation (C7600, "register count of 7").
+  if constexpr (CL > 1) {
+    if (tid == 0 && crank != 0) s_super = remote_ld(&s_super, 0);
+    __syncthreads();
+  }
+  const uint32_t super = s_super;
+  const uint32_t tile = super * CL + crank;
   const uint32_t tile_start = tile * P.tile_keys;
-  const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
+  const uint32_t valid = tile < P.num_tiles ? min(P.tile_keys, P.strip_n - tile_start) : 0u;
   const bool full = valid == uint32_t(TILE);
   const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
   const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
 
   // ---- 2. TMA bulk stage ----------------------------------------------------
-  const bool tma_k = ((reinterpret_cast<uintptr_t>(gk) & 15u) == 0) &&
-                     (((valid * sizeof(K)) & 15u) == 0);
+  // (a tile past the end of the strip -- the tail of the last cluster -- has
+  // valid == 0 and takes the copy path, which then moves nothing)
+  const uint32_t tma_bytes_k = valid * uint32_t(sizeof(K));
+  const bool tma_k = ((reinterpret_cast<uintptr_t>(gk) | tma_bytes_k) & 15u) == 0 && tma_bytes_k;
   bool tma_v = false;
-  if (HAS_V)
-    tma_v = ((reinterpret_cast<uintptr_t>(gv) & 15u) == 0) && (((valid * sizeof(VS)) & 15u) == 0);
+  if (HAS_V) {
+    const uint32_t tma_bytes_v = valid * uint32_t(sizeof(VS));
+    tma_v = ((reinterpret_cast<uintptr_t>(gv) | tma_bytes_v) & 15u) == 0 && tma_bytes_v;
+  }
   if (tid == 0) {
     if (tma_k) {
       mbar_arrive_expect_tx(&s_bar_k, valid * sizeof(K));
@@ -210,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     rank_items(std::false_type{});
   __syncthreads();
 
-  // ---- 4a. tile counts, publish L, local digit starts ------------------------
+  // ---- 4a. tile counts (read by the leader), local digit starts ---------------
   uint32_t count = 0;
   if (tid < radix) {
     uint32_t sum = 0;
@@ -218,9 +276,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
     count = sum;
-    st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
-                   (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
-    if (count == valid) s_fast = tid;
+    s_count[tid] = count;
+    if (valid > 0 && count == valid) s_fast = tid;
   }
   // block-wide exclusive scan of counts over digits (first 8 warps)
   uint32_t incl = count;
@@ -230,7 +287,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     if (lane >= o) incl += t;
   }
   if (lane == 31 && warp < kMaxRadix / 32) s_wsum[warp] = incl;
-  __syncthreads();
+  cluster_sync();  // every CTA's s_count is now visible to the leader
+
+  // leader: publish L for the super-tile right away
+  uint32_t scount = 0;
+  if (crank == 0 && tid < radix) {
+#pragma unroll
+    for (int r = 0; r < CL; ++r) scount += remote_ld(s_count + tid, r);
+    st_relaxed_gpu(P.status + size_t(super) * radix + tid,
+                   (super == 0 ? kFlagGlobal : kFlagLocal) | scount);
+  }
   uint32_t local_start = 0;
   if (tid < radix) {
     uint32_t wpre = 0;
@@ -282,18 +348,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       stage(std::false_type{});
   }
 
-  // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
-  // A new tile starts every ~30 ns while a status round trip through L2 takes
-  // ~0.5-1 us, so the most recent G is typically 15-30 tiles back: each round
-  // trip therefore reads kLookbackWindow predecessor words at once (one
-  // look-back instead of several when the window was 4).  Then publish G and
-  // the per-digit output bases.
-  if (tid < radix) {
+  // ---- 4b. leader: decoupled look-back over super-tiles (lookback.py:144-169),
+  // publish G, hand every CTA its per-digit global bases ----------------------
+  if (crank == 0 && tid < radix) {
     uint32_t excl = 0;
-    uint32_t reads = 0;
-    if (tile > 0) {
+    uint32_t reads = 0, waits = 0, rounds = 0;
+    if (super > 0) {
       const uint32_t* col = P.status + tid;
-      int j = int(tile) - 1;
+      int j = int(super) - 1;
       bool done = false;
       while (!done) {
         uint32_t w[kLookbackWindow];
@@ -301,11 +363,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         for (int k = 0; k < kLookbackWindow; ++k)
           w[k] = (j - k >= 0) ? ld_relaxed_gpu(col + size_t(j - k) * radix) : kFlagGlobal;
         reads += kLookbackWindow;
+        ++rounds;
         int k = 0;
 #pragma unroll
         for (; k < kLookbackWindow; ++k) {
           const uint32_t st = w[k] >> kStatusShift;
-          if (st == 0u) break;  // predecessor in flight: re-poll from here
+          if (st == 0u) {  // predecessor in flight: re-poll from here
+            ++waits;
+            break;
+          }
           excl += w[k] & kValueMask;
           if (st == 2u) {
             done = true;
@@ -314,14 +380,34 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         }
         j -= k;
       }
-      st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
+      st_relaxed_gpu(P.status + size_t(super) * radix + tid, kFlagGlobal | (excl + scount));
     }
-    const unsigned long long gbase = P.base_offsets[tid] + excl;
+    const unsigned long long base = P.base_offsets[tid] + excl;
+    unsigned long long run = base;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      remote_st(s_gbase + tid, r, run);
+      run += remote_ld(s_count + tid, r);
+    }
+    const uint32_t last_super = (P.num_tiles + CL - 1) / CL - 1;
+    if (P.carry_out != nullptr && super == last_super) P.carry_out[tid] = base + scount;
+    if (P.stats != nullptr) {
+      atomicAdd(&s_reads, reads);
+      atomicAdd(&s_waits, waits);
+      atomicAdd(&s_rounds, rounds);
+    }
+  }
+  cluster_sync();  // s_gbase written by the leader
+
+  if (tid < radix) {
+    const unsigned long long gbase = s_gbase[tid];
     const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
     s_kptr[tid] = reinterpret_cast<unsigned long long>(P.dst_keys) + rel * sizeof(K);
     if (HAS_V) s_vptr[tid] = reinterpret_cast<unsigned long long>(P.dst_vals) + rel * sizeof(VS);
-    if (P.carry_out != nullptr && tile == P.num_tiles - 1) P.carry_out[tid] = gbase + count;
-    if (P.stats != nullptr) atomicAdd(&s_reads, reads);
+    // final per-tile word in the reference's CounterMatrix format
+    if (P.tile_status != nullptr && valid > 0)
+      P.tile_status[size_t(tile) * radix + tid] =
+          kFlagGlobal | uint32_t(gbase + count - P.base_offsets[tid]);
   }
   __syncthreads();
 
@@ -333,8 +419,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
-        out_k[idx] = CODED ? cout(keys[i]) : keys[i];
-        if (HAS_V) out_v[idx] = vals[i];
+        st_global(out_k + idx, CODED ? cout(keys[i]) : keys[i]);
+        if (HAS_V) st_global(out_v + idx, vals[i]);
       }
     }
   } else {
@@ -355,8 +441,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   if (P.stats != nullptr && tid == 0) {
     if (fast >= 0) atomicAdd(&P.stats[0], 1ull);
-    atomicAdd(&P.stats[1], (unsigned long long)s_reads);
-    atomicAdd(&P.stats[2], 1ull);
+    if (valid > 0) atomicAdd(&P.stats[2], 1ull);
+    if (crank == 0) {
+      atomicAdd(&P.stats[1], (unsigned long long)s_reads);
+      atomicAdd(&P.stats[3], (unsigned long long)s_waits);
+      atomicAdd(&P.stats[4], (unsigned long long)s_rounds);
+    }
   }
 }
 
@@ -364,8 +454,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
 template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
 static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
+  constexpr int CL = kClusterTiles;
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
-  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED>;
+  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED, CL>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -374,17 +465,32 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     configured = true;
   }
   if (p.num_tiles == 0) return cudaSuccess;
-  kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
-  return cudaGetLastError();
+  const unsigned supers = (p.num_tiles + CL - 1) / CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(supers * CL);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = Smem::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 // Tile geometry per (key, value) width.  THREADS x ITEMS keys per tile; the
 // shared-memory footprint decides how many tiles an SM keeps in flight.
 template <int KB, int VB> struct Geometry;
 #ifndef OS_U32_MINB
-#define OS_U32_MINB 2
+#define OS_U32_MINB 3
 #endif
-template <> struct Geometry<4, 0> { static constexpr int T = 512, I = 16, B = OS_U32_MINB; };
+#ifndef OS_U32_ITEMS
+#define OS_U32_ITEMS 16
+#endif
+template <> struct Geometry<4, 0> { static constexpr int T = 512, I = OS_U32_ITEMS, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 4> { static constexpr int T = 512, I = 16, B = 2; };

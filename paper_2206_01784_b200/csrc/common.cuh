@@ -146,6 +146,31 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---- thread-block clusters: rank, barrier, DSMEM ---------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of this CTA's `p` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem_u64(uint32_t addr, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
 // ---- mbarrier + TMA bulk copy (global -> shared) ---------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
@@ -198,8 +223,9 @@ struct PassParams {
   unsigned long long cout_m0, cout_m1;  // XorCodec applied on store
   const unsigned long long* base_offsets;  // [radix]
   unsigned long long* carry_out;           // [radix] or null
-  uint32_t* status;                        // [num_tiles][radix], zeroed
-  uint32_t* tile_counter;                  // zeroed
+  uint32_t* status;       // look-back words [super-tiles][radix], zeroed
+  uint32_t* tile_status;  // optional final per-tile words [num_tiles][radix] (CounterMatrix view)
+  uint32_t* tile_counter; // super-tile ticket, zeroed
   unsigned long long* stats;               // os_device_stats or null
   const uint8_t* digit_map;                // [2^map_bits] -> destination, or null
 };
@@ -218,6 +244,12 @@ struct HistParams {
 };
 
 // Host launchers (defined in the .cu files).
+// Tiles per cluster: a cluster of kClusterTiles CTAs bins kClusterTiles
+// consecutive tiles and runs one decoupled look-back for the whole super-tile.
+#ifndef OS_CLUSTER_TILES
+#define OS_CLUSTER_TILES 4
+#endif
+constexpr int kClusterTiles = OS_CLUSTER_TILES;
 cudaError_t launch_binning_pass(const PassParams& p, int key_bytes, int val_bytes,
                                 cudaStream_t stream);
 int binning_tile_capacity(int key_bytes, int val_bytes);

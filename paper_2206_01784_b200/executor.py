@@ -120,7 +120,7 @@ class Executor:
     def _drain(self) -> None:
         pending, self._pending = self._pending, []
         for phase, stats, radix in pending:
-            fast, reads, tiles = (int(x) for x in stats.view(__import__("torch").int64).tolist())
+            fast, reads, tiles = (int(x) for x in stats.view(__import__("torch").int64).tolist()[:3])
             counts = self._ledger.setdefault(phase, LedgerCounts())
             counts.fast_path_tiles += fast
             counts.counter_ops += 2 * radix * tiles + reads
