@@ -74,15 +74,6 @@ struct Tiling {
     return (n - lo) < strip ? (n - lo) : strip;
   }
   size_t strip_tiles(size_t s) const { return (strip_len(s) + tile - 1) / tile; }
-  // look-back granules: clusters of kClusterTiles consecutive tiles
-  size_t strip_supers(size_t s) const {
-    return (strip_tiles(s) + kClusterTiles - 1) / kClusterTiles;
-  }
-  size_t supers_total() const {
-    size_t t = 0;
-    for (size_t s = 0; s < strips; ++s) t += strip_supers(s);
-    return t;
-  }
 };
 
 Tiling make_tiling(size_t n, uint32_t tile, size_t strip) {
@@ -116,8 +107,8 @@ int resolve_strip(size_t strip_keys, size_t* out) {
 }
 
 // Workspace of one pass over all strips: look-back status words (one row per
-// super-tile), tile tickets and the 64-bit carries chained between strips
-// (binning.py:196-198, 262).
+// tile, the reference's CounterMatrix layout), tile tickets and the 64-bit
+// carries chained between strips (binning.py:196-198, 262).
 struct PassWs {
   size_t status_words = 0;
   size_t off_status = 0, off_counters = 0, off_carry = 0, bytes = 0, zero_bytes = 0;
@@ -125,7 +116,7 @@ struct PassWs {
 
 PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
   PassWs w;
-  w.status_words = t.supers_total() * size_t(radix);
+  w.status_words = t.tiles_total * size_t(radix);
   size_t off = 0;
   w.off_status = off;
   if (own_status) off = align_up(off + w.status_words * 4);
@@ -146,7 +137,7 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
              const PassWs& w, unsigned long long* stats, cudaStream_t stream) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
   unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
-  size_t tile_base = 0, super_base = 0;
+  size_t tile_base = 0;
   const unsigned long long* base = base0;
   for (size_t s = 0; s < t.strips; ++s) {
     PassParams p{};
@@ -171,7 +162,7 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.base_offsets = base;
     const bool last = (s + 1 == t.strips);
     p.carry_out = last ? carry_final : carries + s * size_t(radix);
-    p.status = status + super_base * size_t(radix);
+    p.status = status + tile_base * size_t(radix);
     p.tile_status = tile_status ? tile_status + tile_base * size_t(radix) : nullptr;
     p.tile_counter = counters + s;
     p.stats = stats;
@@ -179,7 +170,6 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
     tile_base += p.num_tiles;
-    super_base += t.strip_supers(s);
   }
   return OS_OK;
 }

@@ -184,6 +184,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t addr = smem_u32(bar);
@@ -244,12 +252,6 @@ struct HistParams {
 };
 
 // Host launchers (defined in the .cu files).
-// Tiles per cluster: a cluster of kClusterTiles CTAs bins kClusterTiles
-// consecutive tiles and runs one decoupled look-back for the whole super-tile.
-#ifndef OS_CLUSTER_TILES
-#define OS_CLUSTER_TILES 4
-#endif
-constexpr int kClusterTiles = OS_CLUSTER_TILES;
 cudaError_t launch_binning_pass(const PassParams& p, int key_bytes, int val_bytes,
                                 cudaStream_t stream);
 int binning_tile_capacity(int key_bytes, int val_bytes);
