@@ -156,6 +156,12 @@ int os_sort_events(const void* keys_in, void* keys_out, const void* vals_in, voi
                    size_t workspace_bytes, os_device_stats* stats, void** events,
                    int num_events, void* stream);
 
+/* Diagnostics: while buf is non-NULL, binning pass `pass` of later os_sort
+ * calls writes one record of 8 u64 per tile into buf (tile-indexed):
+ * globaltimer ns at claim, keys staged, L published, reorder done, warp 0's
+ * G published, warp 0 done, then the SM id.  Used by tools/trace_diag.py. */
+int os_debug_trace(unsigned long long* buf, int pass);
+
 /* ---- multi-GPU MSD splitter (no reference counterpart) -------
  * Counts the top digit (bits [end_bit - digit_bits, end_bit) of the encoded
  * key) into hist_out u64[2^digit_bits] (overwritten). */

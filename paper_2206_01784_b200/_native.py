@@ -50,6 +50,7 @@ SIGNATURES = {
     "os_sort": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _i, _i, _sz, _vp, _sz, _vp, _vp]),
     "os_sort_events": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _i, _i, _sz, _vp, _sz, _vp,
                             ctypes.POINTER(_vp), _i, _vp]),
+    "os_debug_trace": (_i, [_vp, _i]),
     "os_msd_histogram": (_i, [_vp, _sz, _i, _i, _i, _vp, _vp]),
     "os_msd_partition_workspace_bytes": (_sz, [_sz]),
     "os_msd_partition": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),

@@ -5,6 +5,7 @@
 // element work -- there is no host compute path.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/onesweep_b200.h"
@@ -111,12 +112,14 @@ int resolve_strip(size_t strip_keys, size_t* out) {
 // carries chained between strips (binning.py:196-198, 262).
 struct PassWs {
   size_t status_words = 0;
+  size_t strip_status_words = 0;  // every strip uses the stride of a full strip
   size_t off_status = 0, off_counters = 0, off_carry = 0, bytes = 0, zero_bytes = 0;
 };
 
 PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
   PassWs w;
-  w.status_words = t.tiles_total * size_t(radix);
+  w.strip_status_words = t.strips ? status_words_for(t.strip_tiles(0), radix) : 0;
+  w.status_words = t.strips * w.strip_status_words;
   size_t off = 0;
   w.off_status = off;
   if (own_status) off = align_up(off + w.status_words * 4);
@@ -129,12 +132,29 @@ PassWs pass_ws(const Tiling& t, int radix, bool own_status) {
   return w;
 }
 
+// L2 prefetch distance of the binning kernel, in tiles: about one wave of
+// resident blocks ahead (ONESWEEP_B200_PREFETCH overrides; 0 disables).
+uint32_t prefetch_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ONESWEEP_B200_PREFETCH");
+    v = e ? atoi(e) : 296;
+    if (v < 0) v = 0;
+  }
+  return uint32_t(v);
+}
+
+// Diagnostics (os_debug_trace): per-tile timeline of one pass.
+unsigned long long* g_trace = nullptr;
+int g_trace_pass = -1;
+
 // One binning pass over every strip (partition_pass, binning.py:218-275).
 int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int kb, int vb,
              const Tiling& t, int shift, int width, int radix, const uint8_t* digit_map,
              const unsigned long long* base0, unsigned long long* carry_final, int codec_in,
              int codec_out, uint32_t* status, uint32_t* tile_status, unsigned char* ws,
-             const PassWs& w, unsigned long long* stats, cudaStream_t stream) {
+             const PassWs& w, unsigned long long* stats, cudaStream_t stream,
+             unsigned long long* trace = nullptr) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
   unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
   size_t tile_base = 0;
@@ -162,11 +182,13 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.base_offsets = base;
     const bool last = (s + 1 == t.strips);
     p.carry_out = last ? carry_final : carries + s * size_t(radix);
-    p.status = status + tile_base * size_t(radix);
+    p.status = status + s * w.strip_status_words;
     p.tile_status = tile_status ? tile_status + tile_base * size_t(radix) : nullptr;
     p.tile_counter = counters + s;
     p.stats = stats;
     p.digit_map = digit_map;
+    p.prefetch_tiles = prefetch_tiles();
+    p.trace = trace ? trace + tile_base * kTraceWords : nullptr;
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
     tile_base += p.num_tiles;
@@ -449,7 +471,8 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
     int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
                       offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
                       k == L.passes - 1 ? kt.dec : CODEC_NONE, status, nullptr, pws, L.pw,
-                      reinterpret_cast<unsigned long long*>(stats), s);
+                      reinterpret_cast<unsigned long long*>(stats), s,
+                      k == g_trace_pass ? g_trace : nullptr);
     if (rc) return rc;
     OS_CUDA(mark(2 + k), "event");
     src_k = dst_k;
@@ -479,6 +502,12 @@ int os_sort_events(const void* keys_in, void* keys_out, const void* vals_in, voi
   return sort_impl(keys_in, keys_out, vals_in, vals_out, n, key_type, val_bytes, digit_bits,
                    begin_bit, end_bit, tile_keys, strip_keys, workspace, workspace_bytes, stats,
                    events, num_events, stream);
+}
+
+int os_debug_trace(unsigned long long* buf, int pass) {
+  g_trace = buf;
+  g_trace_pass = buf ? pass : -1;
+  return OS_OK;
 }
 
 int os_msd_histogram(const void* keys, size_t n, int key_type, int digit_bits, int end_bit,

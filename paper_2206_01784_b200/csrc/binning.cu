@@ -47,6 +47,113 @@ template <> struct ValTraits<NoValue> {
 #define OS_LOOKBACK_WINDOW 4
 #endif
 constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
+// 1: inclusive ranks stored by the highest peer, packed with PRMT, counters
+// addressed from a per-warp shared base (fewer instructions per item).
+#ifndef OS_RANK_V2
+#define OS_RANK_V2 1
+#endif
+// Look-back layout.  0: status words tile-major ([tile][digit], the
+// reference's CounterMatrix), kLookbackWindow scalar loads per round trip.
+// 1: groups of four tiles ([tile/4][digit][tile%4]); a round trip is
+// OS_LB_GROUPS 16-byte loads, i.e. 4*OS_LB_GROUPS predecessors.
+#ifndef OS_LB_VEC
+#define OS_LB_VEC 0
+#endif
+#ifndef OS_LB_GROUPS
+#define OS_LB_GROUPS 2
+#endif
+
+// Scan chaser: the first block of every launch does no tile; it walks the
+// status words in tile order and turns each L|count into G|inclusive as soon
+// as it appears, so a tile's look-back normally meets a G one predecessor
+// back instead of waiting for a convoy of predecessors to finish their own
+// look-backs.  Tiles keep the full decoupled look-back (and still publish G
+// themselves), so the chaser only shortens it.
+#ifndef OS_CHASER
+#define OS_CHASER 0
+#endif
+#ifndef OS_CHASER_BATCH
+#define OS_CHASER_BATCH 16  // tiles per lane per round trip (two lanes per digit)
+#endif
+#ifndef OS_CHASER_BACKOFF_NS
+#define OS_CHASER_BACKOFF_NS 64
+#endif
+
+// Status word of (tile t, digit d) in one strip's status array.
+__device__ __forceinline__ size_t status_word(uint32_t t, int d, int radix) {
+  return OS_LB_VEC ? size_t(t >> 2) * (size_t(radix) * 4) + size_t(d) * 4 + (t & 3u)
+                   : size_t(t) * radix + d;
+}
+
+template <int THREADS>
+__device__ void scan_chaser(const PassParams& P) {
+  static_assert(THREADS / 2 >= kMaxRadix, "two lanes per digit");
+  constexpr int B = OS_CHASER_BATCH;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int d = tid >> 1;
+  const int q = tid & 1;  // lane q covers tiles [t0 + q*B, t0 + (q+1)*B)
+  const int radix = P.radix;
+  const uint32_t nt = P.num_tiles;
+  uint32_t t0 = 0, running = 0;  // running = inclusive count of digit d over tiles < t0
+  bool finished = d >= radix;
+  while (__any_sync(0xffffffffu, !finished)) {
+    const uint32_t base = t0 + uint32_t(q) * B;
+    uint32_t w[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      w[k] = (!finished && base + k < nt) ? ld_relaxed_gpu(P.status + status_word(base + k, d, radix))
+                                          : 0u;
+    // this lane's ready prefix as an affine step: reset to a G value, then add
+    int v = 0;
+    bool reset = false, stop = false;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const uint32_t st = w[k] >> kStatusShift;
+      if (!stop) {
+        if (st == 0u) {
+          stop = true;
+        } else {
+          ++v;
+          if (st == 2u) {
+            reset = true;
+            acc = w[k] & kValueMask;
+          } else {
+            acc += w[k] & kValueMask;
+          }
+        }
+      }
+    }
+    const int pair = lane & ~1;
+    const int v0 = __shfl_sync(0xffffffffu, v, pair);
+    const bool r0 = __shfl_sync(0xffffffffu, int(reset), pair) != 0;
+    const uint32_t a0 = __shfl_sync(0xffffffffu, acc, pair);
+    const bool full0 = v0 == B;
+    const int my_v = (q == 0 || full0) ? v : 0;
+    uint32_t r = q == 0 ? running : (r0 ? a0 : running + a0);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (k < my_v) {
+        const uint32_t st = w[k] >> kStatusShift;
+        const uint32_t val = w[k] & kValueMask;
+        r = st == 2u ? val : r + val;
+        if (st == 1u) st_relaxed_gpu(P.status + status_word(base + k, d, radix), kFlagGlobal | r);
+      }
+    }
+    const uint32_t r_lo = __shfl_sync(0xffffffffu, r, pair);
+    const uint32_t r_hi = __shfl_sync(0xffffffffu, r, pair | 1);
+    const int v1 = __shfl_sync(0xffffffffu, my_v, pair | 1);
+    const uint32_t adv = uint32_t(v0) + (full0 ? uint32_t(v1) : 0u);
+    if (!finished) {
+      running = full0 ? r_hi : r_lo;
+      t0 += adv;
+      if (t0 >= nt) finished = true;
+    }
+    if (OS_CHASER_BACKOFF_NS > 0 && __all_sync(0xffffffffu, finished || adv == 0))
+      __nanosleep(OS_CHASER_BACKOFF_NS);
+  }
+}
 
 template <int THREADS, int ITEMS, int KB, int VB>
 struct BinningSmem {
@@ -63,7 +170,8 @@ struct BinningSmem {
   static constexpr size_t kBytes = kKeys + kVals + kHist + kKPtr + kVPtr + kLocal + kWsum + kMap;
 };
 
-template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
+          bool BYTE>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
   constexpr bool HAS_V = ValTraits<V>::kHas;
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
@@ -101,9 +209,28 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const uint32_t dmask = P.mask;
   const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
   const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
+  // byte-aligned 8-bit digit: one PRMT picks it out of the right 32-bit word
+  const uint32_t byte_sel = 0x4440u | uint32_t((shift & 31) >> 3);
+  const bool hi_word = shift >= 32;
 
   if (tid == 0) {
-    s_tile = atomicAdd(P.tile_counter, 1u);
+    // ticket 0 is the scan chaser (when enabled); tiles are tickets 1..
+    const uint32_t t = atomicAdd(P.tile_counter, 1u) - (OS_CHASER ? 1u : 0u);
+    s_tile = t;
+    // warm L2 with a tile that a block starting a few microseconds from now
+    // will claim; its TMA then hits L2 instead of waiting on HBM
+    const uint32_t pf = t + P.prefetch_tiles;
+    if (t != 0xffffffffu && P.prefetch_tiles != 0 && pf + 1 < P.num_tiles) {
+      const size_t off = size_t(pf) * P.tile_keys;
+      const K* pk = static_cast<const K*>(P.src_keys) + off;
+      if ((reinterpret_cast<uintptr_t>(pk) & 15u) == 0 && ((P.tile_keys * sizeof(K)) & 15u) == 0)
+        l2_prefetch(pk, P.tile_keys * sizeof(K));
+      if (HAS_V) {
+        const VS* pv = static_cast<const VS*>(P.src_vals) + off;
+        if ((reinterpret_cast<uintptr_t>(pv) & 15u) == 0 && ((P.tile_keys * sizeof(VS)) & 15u) == 0)
+          l2_prefetch(pv, P.tile_keys * sizeof(VS));
+      }
+    }
     s_fast = -1;
     s_reads = s_waits = s_rounds = 0;
     mbar_init(&s_bar_k, 1);
@@ -121,9 +248,18 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   __syncthreads();
 
   const uint32_t tile = s_tile;
+  if constexpr (OS_CHASER && THREADS / 2 >= kMaxRadix) {
+    if (tile == 0xffffffffu) {
+      scan_chaser<THREADS>(P);
+      return;
+    }
+  }
   const uint32_t tile_start = tile * P.tile_keys;
+  unsigned long long* trace = P.trace ? P.trace + size_t(tile) * kTraceWords : nullptr;
+  if (trace && tid == 0) { trace[0] = global_ns(); trace[6] = smid(); }
   const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
   const bool full = valid == uint32_t(TILE);
+  auto status_index = [&](uint32_t t, int d) -> size_t { return status_word(t, d, radix); };
   const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
   const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
 
@@ -165,13 +301,24 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   }
   if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+  if (trace && tid == 0) trace[1] = global_ns();
 
   auto load_key = [&](uint32_t idx) -> K {
     const K x = s_keys[idx];
     return CODED ? cin(x) : x;
   };
   auto digit = [&](K x) -> uint32_t {
-    uint32_t d = digit_of(x, shift, dmask);
+    uint32_t d;
+    if (BYTE) {
+      uint32_t w;
+      if constexpr (sizeof(K) == 8)
+        w = hi_word ? uint32_t(uint64_t(x) >> 32) : uint32_t(x);
+      else
+        w = uint32_t(x);
+      d = __byte_perm(w, 0u, byte_sel);
+    } else {
+      d = digit_of(x, shift, dmask);
+    }
     if (MAPPED) d = s_map[d];
     return d;
   };
@@ -184,6 +331,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     uint32_t* my_hist = s_whist + warp * kMaxRadix;
+    const uint32_t hbase = smem_u32(my_hist);
+    (void)hbase;
+    (void)my_hist;
     const uint32_t lt = lanemask_lt();
     const uint32_t le = lt | (1u << lane);
 #pragma unroll
@@ -194,6 +344,22 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         d = digit(load_key(idx));
       else
         d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
+#if OS_RANK_V2
+      // inclusive rank (own slot counted); the highest peer stores it as the
+      // digit's new running count
+      uint32_t upto;
+      bool leader;
+      match_rank8(d, le, ~le, &upto, &leader);
+      const uint32_t caddr = hbase + d * 4u;
+      const uint32_t rank = lds_u32(caddr) + __popc(upto);
+      if (i & 1)
+        ranks[i / 2] = __byte_perm(ranks[i / 2], rank, 0x5410);
+      else
+        ranks[i / 2] = rank;
+      __syncwarp();
+      if (leader) sts_u32(caddr, rank);
+      __syncwarp();
+#else
       const uint32_t peers = match_peers8(d);
       const uint32_t rank = my_hist[d] + __popc(peers & lt);
       if (i & 1)
@@ -203,6 +369,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       __syncwarp();
       if (peers <= le) my_hist[d] = rank + 1;  // highest peer: count after this batch
       __syncwarp();
+#endif
     }
   };
   if (full)
@@ -219,10 +386,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
     count = sum;
-    st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
-                   (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    st_relaxed_gpu(P.status + status_index(tile, tid), (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
+  if (trace && tid == 0) trace[2] = global_ns();
   // block-wide exclusive scan of counts over digits (first 8 warps)
   uint32_t incl = count;
 #pragma unroll
@@ -240,7 +407,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     s_local[tid] = local_start;
     // fold the tile-local start into every warp's exclusive offset so the
     // reorder needs a single shared-memory gather per key
-    uint32_t run = local_start;
+    uint32_t run = local_start - (OS_RANK_V2 ? 1u : 0u);  // ranks are inclusive in V2
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const uint32_t c = s_whist[w * kMaxRadix + tid];
@@ -283,6 +450,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       stage(std::false_type{});
   }
 
+  if (trace && tid == 0) trace[3] = global_ns();
   // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
   // A new tile starts every ~30 ns while a status round trip through L2 takes
   // ~0.5-1 us, so the most recent G is typically 15-30 tiles back: each round
@@ -292,7 +460,48 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
-    if (tile > 0) {
+    if (tile > 0 && OS_LB_VEC) {
+      // groups of four predecessors, OS_LB_GROUPS 16-byte loads per round trip
+      const uint32_t* col = P.status + size_t(tid) * 4;
+      const size_t gstride = size_t(radix) * 4;
+      int j = int(tile) - 1;  // next predecessor to add
+      bool done = false;
+      while (!done) {
+        const int g = j >> 2;
+        uint4 w[OS_LB_GROUPS];
+#pragma unroll
+        for (int k = 0; k < OS_LB_GROUPS; ++k)
+          w[k] = g - k >= 0 ? ld_relaxed_gpu_v4(col + size_t(g - k) * gstride)
+                            : make_uint4(kFlagGlobal, kFlagGlobal, kFlagGlobal, kFlagGlobal);
+        reads += 4 * OS_LB_GROUPS;
+        ++rounds;
+        int next = (g - OS_LB_GROUPS + 1) * 4 - 1;
+        bool stop = false;
+#pragma unroll
+        for (int k = 0; k < OS_LB_GROUPS; ++k) {
+          const uint32_t w4[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+          for (int e = 3; e >= 0; --e) {
+            const int pos = (g - k) * 4 + e;
+            if (!stop && pos <= j) {
+              const uint32_t x = w4[e];
+              if (x & kFlagLocal) {
+                excl += x & kValueMask;
+              } else if (x & kFlagGlobal) {
+                excl += x & kValueMask;
+                stop = done = true;
+              } else {  // predecessor in flight: re-poll from it
+                stop = true;
+                next = pos;
+                ++waits;
+              }
+            }
+          }
+        }
+        j = next;
+      }
+      st_relaxed_gpu(P.status + status_index(tile, tid), kFlagGlobal | (excl + count));
+    } else if (tile > 0) {
       const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
       bool done = false;
@@ -319,8 +528,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         }
         j -= k;
       }
-      st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
+      st_relaxed_gpu(P.status + status_index(tile, tid), kFlagGlobal | (excl + count));
     }
+    if (trace && tid == 0) trace[4] = global_ns();
     const unsigned long long gbase = P.base_offsets[tid] + excl;
     const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
     s_kptr[tid] = reinterpret_cast<unsigned long long>(P.dst_keys) + rel * sizeof(K);
@@ -364,6 +574,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   }
 
+  if (trace && tid == 0) trace[5] = global_ns();
   if (P.stats != nullptr && tid == 0) {
     if (fast >= 0) atomicAdd(&P.stats[0], 1ull);
     atomicAdd(&P.stats[1], (unsigned long long)s_reads);
@@ -375,10 +586,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
 // ---- host side ------------------------------------------------------------------
 
-template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED>
+template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
+          bool BYTE>
 static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
-  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED>;
+  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED, BYTE>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -387,7 +599,7 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     configured = true;
   }
   if (p.num_tiles == 0) return cudaSuccess;
-  kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
+  kern<<<p.num_tiles + (OS_CHASER ? 1 : 0), THREADS, Smem::kBytes, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -395,9 +607,15 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
 // shared-memory footprint decides how many tiles an SM keeps in flight.
 template <int KB, int VB> struct Geometry;
 #ifndef OS_U32_MINB
-#define OS_U32_MINB 3
+#define OS_U32_MINB 4
 #endif
-template <> struct Geometry<4, 0> { static constexpr int T = 512, I = 16, B = OS_U32_MINB; };
+#ifndef OS_U32_THREADS
+#define OS_U32_THREADS 256
+#endif
+#ifndef OS_U32_ITEMS
+#define OS_U32_ITEMS 32
+#endif
+template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 4> { static constexpr int T = 512, I = 16, B = 2; };
@@ -415,9 +633,14 @@ static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
   using G = Geometry<KB, VB>;
   if (p.tile_keys == 0 || p.tile_keys > uint32_t(G::T * G::I)) return cudaErrorInvalidValue;
   const bool coded = (p.cin_m0 | p.cin_m1 | p.cout_m0 | p.cout_m1) != 0;
-  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true, true>(p, stream);
-  if (coded) return launch_one<K, V, G::T, G::I, G::B, false, true>(p, stream);
-  return launch_one<K, V, G::T, G::I, G::B, false, false>(p, stream);
+  const bool byte = (p.shift % 8) == 0 && p.mask == 0xffu;
+  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true, true, false>(p, stream);
+  if (coded) {
+    if (byte) return launch_one<K, V, G::T, G::I, G::B, false, true, true>(p, stream);
+    return launch_one<K, V, G::T, G::I, G::B, false, true, false>(p, stream);
+  }
+  if (byte) return launch_one<K, V, G::T, G::I, G::B, false, false, true>(p, stream);
+  return launch_one<K, V, G::T, G::I, G::B, false, false, false>(p, stream);
 }
 
 template <typename K>
@@ -456,5 +679,8 @@ int binning_tile_capacity(int key_bytes, int val_bytes) {
   if (key_bytes == 8) return capacity_for<8>(val_bytes);
   return 0;
 }
+
+// Status words of one strip (look-back layout, see the kernel).
+size_t status_words_for(size_t tiles, int radix) { return (tiles + 3) / 4 * 4 * size_t(radix); }
 
 }  // namespace osb

@@ -102,6 +102,46 @@ __device__ __forceinline__ uint32_t match_peers8(uint32_t d) {
   return and3(and3(v0, v1, v2), and3(v3, v4, v5), v6 & v7);
 }
 
+// Stable warp rank for an 8-bit digit, with the peer mask folded straight into
+// the two quantities the ranking loop consumes: the lower same-digit lanes
+// (`below`) and whether this lane is the highest of its peers (`leader`).
+// `sel` is the lane mask the peers are counted over (lanemask_lt for an
+// exclusive rank, lanemask_le for an inclusive one); `gt` is lanemask_gt.
+__device__ __forceinline__ void match_rank8(uint32_t d, uint32_t sel, uint32_t gt, uint32_t* peers_sel,
+                                            bool* leader) {
+  const uint32_t v0 = vote_bit(d, 1), v1 = vote_bit(d, 2), v2 = vote_bit(d, 4),
+                 v3 = vote_bit(d, 8), v4 = vote_bit(d, 16), v5 = vote_bit(d, 32),
+                 v6 = vote_bit(d, 64), v7 = vote_bit(d, 128);
+  const uint32_t c = and3(and3(v0, v1, v2), and3(v3, v4, v5), v6);
+  *peers_sel = and3(c, v7, sel);
+  *leader = and3(c, v7, gt) == 0u;
+}
+
+// Shared-memory accesses by 32-bit shared address.  Volatile, so ptxas keeps
+// them in program order relative to each other (the ranking counters are
+// read and rewritten by the same warp item after item), but without a memory
+// clobber, so ordinary loads of other shared data may still be scheduled
+// around them.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+template <typename T>
+__device__ __forceinline__ void sts_val(uint32_t addr, T v) {
+  if constexpr (sizeof(T) == 8)
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"((unsigned long long)v));
+  else if constexpr (sizeof(T) == 4)
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)v));
+  else if constexpr (sizeof(T) == 2)
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+  else
+    asm volatile("st.shared.b8 [%0], %1;" ::"r"(addr), "r"((uint32_t)v));
+}
+
 // keycodec.py:228-239 plus the begin-bit offset: (enc >> shift) & mask.
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K x, int shift, uint32_t mask) {
@@ -117,6 +157,23 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// Four consecutive status words; each element is single-copy atomic, which is
+// all the protocol needs (every word carries its own flag).
+__device__ __forceinline__ uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void named_barrier_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// Bulk L2 prefetch (no shared-memory destination); bytes % 16 == 0.
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -231,12 +288,27 @@ struct PassParams {
   unsigned long long cout_m0, cout_m1;  // XorCodec applied on store
   const unsigned long long* base_offsets;  // [radix]
   unsigned long long* carry_out;           // [radix] or null
-  uint32_t* status;       // look-back words [super-tiles][radix], zeroed
+  uint32_t* status;       // look-back words [tiles/4][radix][4], zeroed
   uint32_t* tile_status;  // optional final per-tile words [num_tiles][radix] (CounterMatrix view)
   uint32_t* tile_counter; // super-tile ticket, zeroed
   unsigned long long* stats;               // os_device_stats or null
   const uint8_t* digit_map;                // [2^map_bits] -> destination, or null
+  uint32_t prefetch_tiles;                 // L2-prefetch distance in tiles (0: off)
+  unsigned long long* trace;               // diagnostics: kTraceWords per tile, or null
 };
+// Per-tile trace record (globaltimer ns): claim, keys staged, L published,
+// reorder done, warp 0 G published, warp 0 done, SM id, unused.
+constexpr int kTraceWords = 8;
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 struct HistParams {
   const void* keys;
@@ -255,6 +327,7 @@ struct HistParams {
 cudaError_t launch_binning_pass(const PassParams& p, int key_bytes, int val_bytes,
                                 cudaStream_t stream);
 int binning_tile_capacity(int key_bytes, int val_bytes);
+size_t status_words_for(size_t tiles, int radix);
 cudaError_t launch_histogram(const HistParams& p, int key_bytes, cudaStream_t stream);
 cudaError_t launch_exclusive_scan(const unsigned long long* counts, int rows, int radix,
                                   unsigned long long* out, cudaStream_t stream);
