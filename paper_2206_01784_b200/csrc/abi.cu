@@ -154,7 +154,7 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
              const unsigned long long* base0, unsigned long long* carry_final, int codec_in,
              int codec_out, uint32_t* status, uint32_t* tile_status, unsigned char* ws,
              const PassWs& w, unsigned long long* stats, cudaStream_t stream,
-             unsigned long long* trace = nullptr) {
+             bool dense_bases, unsigned long long* trace = nullptr) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
   unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
   size_t tile_base = 0;
@@ -188,6 +188,9 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.stats = stats;
     p.digit_map = digit_map;
     p.prefetch_tiles = prefetch_tiles();
+    // the run writes index the output with 32 bits unless it could be larger
+    // (partition_pass callers may pass any base offsets)
+    p.wide_index = !dense_bases || t.n >= (size_t(1) << 32) - (size_t(1) << 26);
     p.trace = trace ? trace + tile_base * kTraceWords : nullptr;
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
@@ -377,7 +380,8 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
     OS_CUDA(cudaMemsetAsync(status_out, 0, t.tiles_total * size_t(radix) * 4, s), "status memset");
   return run_pass(src_keys, dst_keys, src_vals, dst_vals, key_bytes, val_bytes, t, shift,
                   digit_width, radix, nullptr, base_offsets, carry_out, codec_in, codec_out, status,
-                  status_out, ws, w, reinterpret_cast<unsigned long long*>(stats), s);
+                  status_out, ws, w, reinterpret_cast<unsigned long long*>(stats), s,
+                  /*dense_bases=*/false);
 }
 
 size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_bits,
@@ -471,7 +475,7 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
     int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
                       offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
                       k == L.passes - 1 ? kt.dec : CODEC_NONE, status, nullptr, pws, L.pw,
-                      reinterpret_cast<unsigned long long*>(stats), s,
+                      reinterpret_cast<unsigned long long*>(stats), s, /*dense_bases=*/true,
                       k == g_trace_pass ? g_trace : nullptr);
     if (rc) return rc;
     OS_CUDA(mark(2 + k), "event");
@@ -587,7 +591,7 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in, v
   return run_pass(keys_in, keys_out, vals_in, vals_out, kt.bytes, val_bytes, t,
                   end_bit - digit_bits, digit_bits, parts, map, seg_offsets, carry_final, kt.enc,
                   kt.dec, reinterpret_cast<uint32_t*>(pws + w.off_status), nullptr, pws, w, nullptr,
-                  s);
+                  s, /*dense_bases=*/true);
 }
 
 }  // extern "C"

@@ -10,19 +10,27 @@
 // with one CUDA kernel in which a thread block processes one tile:
 //
 //   1. claim a tile id from an atomic ticket (forward progress for the
-//      chained scan: ids are handed out in block-start order, executor.py:1-8);
+//      chained scan: ids are handed out in block-start order, executor.py:1-8)
+//      and prefetch a tile further down the strip into L2;
 //   2. stage the tile's keys (and values) into shared memory with one TMA bulk
 //      copy each (cp.async.bulk ... mbarrier::complete_tx); values land while
 //      the keys are ranked;
 //   3. rank keys with a warp-level multisplit: eight ballots (one per digit
 //      bit) give the same-digit peer mask, rank = warp running count + popc of
-//      lower peers -- the reference's WLMS (_kernels.py:56-82) on VOTE/LOP3;
-//   4. reduce per-warp digit counts to tile counts (thread i owns digit i,
-//      PAPER.md:187), publish L|count, locally reorder the tile into per-digit
-//      runs, then look back over predecessor status words (a window of
-//      predecessors per round trip) and publish G|inclusive;
+//      lower-or-equal peers -- the reference's WLMS (_kernels.py:56-82) on
+//      VOTE/LOP3;
+//   4. reduce per-warp digit counts to tile counts (thread d owns digit d,
+//      PAPER.md:187), publish L|count, reorder the tile in place into
+//      per-digit runs, then look back over predecessor status words and
+//      publish G|inclusive;
 //   5. write each run with coalesced stores at base + exclusive + (slot -
 //      start); the codec (signed/float decode) is applied on the way out.
+//
+// The pass is bound by the SM's shared-memory/L1 data pipe, not by HBM
+// (profiles/round1_ncu_summary.md): every digit-indexed table access by 32
+// random digits costs ~3 bank wavefronts.  The layout choices below trade
+// instructions for wavefronts: 16-bit per-warp counters (two digits per
+// bank word) and a 32-bit output-index table for the run writes.
 //
 // Keys move once in and once out: 2n element transfers per pass, the
 // reference's ledger identity (binning.py:268-272).
@@ -43,117 +51,18 @@ template <> struct ValTraits<NoValue> {
   static constexpr int kBytes = 0;
 };
 
+// Predecessor status words read per look-back round trip (lookback.py:144-169).
 #ifndef OS_LOOKBACK_WINDOW
 #define OS_LOOKBACK_WINDOW 4
 #endif
 constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
-// 1: inclusive ranks stored by the highest peer, packed with PRMT, counters
-// addressed from a per-warp shared base (fewer instructions per item).
-#ifndef OS_RANK_V2
-#define OS_RANK_V2 1
-#endif
-// Look-back layout.  0: status words tile-major ([tile][digit], the
-// reference's CounterMatrix), kLookbackWindow scalar loads per round trip.
-// 1: groups of four tiles ([tile/4][digit][tile%4]); a round trip is
-// OS_LB_GROUPS 16-byte loads, i.e. 4*OS_LB_GROUPS predecessors.
-#ifndef OS_LB_VEC
-#define OS_LB_VEC 0
-#endif
-#ifndef OS_LB_GROUPS
-#define OS_LB_GROUPS 2
+// 1: keys stay in registers from the ranking loop to the reorder (one shared
+// load per key less, more registers); 0: re-read before the reorder.
+#ifndef OS_KEYS_IN_REGS
+#define OS_KEYS_IN_REGS 0
 #endif
 
-// Scan chaser: the first block of every launch does no tile; it walks the
-// status words in tile order and turns each L|count into G|inclusive as soon
-// as it appears, so a tile's look-back normally meets a G one predecessor
-// back instead of waiting for a convoy of predecessors to finish their own
-// look-backs.  Tiles keep the full decoupled look-back (and still publish G
-// themselves), so the chaser only shortens it.
-#ifndef OS_CHASER
-#define OS_CHASER 0
-#endif
-#ifndef OS_CHASER_BATCH
-#define OS_CHASER_BATCH 16  // tiles per lane per round trip (two lanes per digit)
-#endif
-#ifndef OS_CHASER_BACKOFF_NS
-#define OS_CHASER_BACKOFF_NS 64
-#endif
-
-// Status word of (tile t, digit d) in one strip's status array.
-__device__ __forceinline__ size_t status_word(uint32_t t, int d, int radix) {
-  return OS_LB_VEC ? size_t(t >> 2) * (size_t(radix) * 4) + size_t(d) * 4 + (t & 3u)
-                   : size_t(t) * radix + d;
-}
-
-template <int THREADS>
-__device__ void scan_chaser(const PassParams& P) {
-  static_assert(THREADS / 2 >= kMaxRadix, "two lanes per digit");
-  constexpr int B = OS_CHASER_BATCH;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int d = tid >> 1;
-  const int q = tid & 1;  // lane q covers tiles [t0 + q*B, t0 + (q+1)*B)
-  const int radix = P.radix;
-  const uint32_t nt = P.num_tiles;
-  uint32_t t0 = 0, running = 0;  // running = inclusive count of digit d over tiles < t0
-  bool finished = d >= radix;
-  while (__any_sync(0xffffffffu, !finished)) {
-    const uint32_t base = t0 + uint32_t(q) * B;
-    uint32_t w[B];
-#pragma unroll
-    for (int k = 0; k < B; ++k)
-      w[k] = (!finished && base + k < nt) ? ld_relaxed_gpu(P.status + status_word(base + k, d, radix))
-                                          : 0u;
-    // this lane's ready prefix as an affine step: reset to a G value, then add
-    int v = 0;
-    bool reset = false, stop = false;
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      const uint32_t st = w[k] >> kStatusShift;
-      if (!stop) {
-        if (st == 0u) {
-          stop = true;
-        } else {
-          ++v;
-          if (st == 2u) {
-            reset = true;
-            acc = w[k] & kValueMask;
-          } else {
-            acc += w[k] & kValueMask;
-          }
-        }
-      }
-    }
-    const int pair = lane & ~1;
-    const int v0 = __shfl_sync(0xffffffffu, v, pair);
-    const bool r0 = __shfl_sync(0xffffffffu, int(reset), pair) != 0;
-    const uint32_t a0 = __shfl_sync(0xffffffffu, acc, pair);
-    const bool full0 = v0 == B;
-    const int my_v = (q == 0 || full0) ? v : 0;
-    uint32_t r = q == 0 ? running : (r0 ? a0 : running + a0);
-#pragma unroll
-    for (int k = 0; k < B; ++k) {
-      if (k < my_v) {
-        const uint32_t st = w[k] >> kStatusShift;
-        const uint32_t val = w[k] & kValueMask;
-        r = st == 2u ? val : r + val;
-        if (st == 1u) st_relaxed_gpu(P.status + status_word(base + k, d, radix), kFlagGlobal | r);
-      }
-    }
-    const uint32_t r_lo = __shfl_sync(0xffffffffu, r, pair);
-    const uint32_t r_hi = __shfl_sync(0xffffffffu, r, pair | 1);
-    const int v1 = __shfl_sync(0xffffffffu, my_v, pair | 1);
-    const uint32_t adv = uint32_t(v0) + (full0 ? uint32_t(v1) : 0u);
-    if (!finished) {
-      running = full0 ? r_hi : r_lo;
-      t0 += adv;
-      if (t0 >= nt) finished = true;
-    }
-    if (OS_CHASER_BACKOFF_NS > 0 && __all_sync(0xffffffffu, finished || adv == 0))
-      __nanosleep(OS_CHASER_BACKOFF_NS);
-  }
-}
+constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
 
 template <int THREADS, int ITEMS, int KB, int VB>
 struct BinningSmem {
@@ -161,37 +70,39 @@ struct BinningSmem {
   static constexpr int kWarps = THREADS / 32;
   static constexpr size_t kKeys = size_t(kTile) * KB;
   static constexpr size_t kVals = (size_t(kTile) * VB + 15) / 16 * 16;
-  static constexpr size_t kHist = size_t(kWarps) * kMaxRadix * 4;  // per-warp digit counters
-  static constexpr size_t kKPtr = kMaxRadix * 8;  // per-digit output base address (keys)
-  static constexpr size_t kVPtr = VB ? kMaxRadix * 8 : 0;  // (values)
+  // per-warp u16 digit counters, later the warp's slot offsets
+  static constexpr size_t kHist = (size_t(kWarps) * kMaxRadix * 2 + 15) / 16 * 16;
+  static constexpr size_t kPtr = kMaxRadix * 8;  // per-digit 64-bit output index (keys, values)
+  static constexpr size_t kRel = kMaxRadix * 4;  // per-digit 32-bit output index
   static constexpr size_t kLocal = kMaxRadix * 4;  // tile-local digit starts
   static constexpr size_t kWsum = 32 * 4;
   static constexpr size_t kMap = kMaxRadix;
-  static constexpr size_t kBytes = kKeys + kVals + kHist + kKPtr + kVPtr + kLocal + kWsum + kMap;
+  static constexpr size_t kBytes = kKeys + kVals + kHist + kPtr + kRel + kLocal + kWsum + kMap;
 };
 
 template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
           bool BYTE>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
   constexpr bool HAS_V = ValTraits<V>::kHas;
-  using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
+  constexpr int KB = sizeof(K);
+  using Smem = BinningSmem<THREADS, ITEMS, KB, ValTraits<V>::kBytes>;
   constexpr int TILE = Smem::kTile;
   constexpr int WARPS = Smem::kWarps;
   static_assert(THREADS >= kMaxRadix, "one thread per digit for the look-back");
   static_assert(THREADS % 32 == 0, "whole warps");
-  static_assert(TILE < 65536, "ranks are packed as u16");
-  static_assert((WARPS * kMaxRadix) % (4 * THREADS) == 0, "vectorised counter reset");
+  static_assert(TILE * KB <= 65536, "u16 slot offsets");
+  static_assert(32 * ITEMS * KB < 65536, "u16 scaled per-warp counters");
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
+  constexpr int VB = HAS_V ? int(sizeof(VS)) : 0;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   VS* s_vals = reinterpret_cast<VS*>(smem_raw + Smem::kKeys);
-  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem_raw + Smem::kKeys + Smem::kVals);
-  unsigned long long* s_kptr = reinterpret_cast<unsigned long long*>(
+  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem_raw + Smem::kKeys + Smem::kVals);
+  unsigned long long* s_ptr = reinterpret_cast<unsigned long long*>(
       smem_raw + Smem::kKeys + Smem::kVals + Smem::kHist);
-  unsigned long long* s_vptr = s_kptr + kMaxRadix;  // only when HAS_V
-  uint32_t* s_local = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(s_kptr) +
-                                                  Smem::kKPtr + Smem::kVPtr);
+  uint32_t* s_rel = reinterpret_cast<uint32_t*>(s_ptr + kMaxRadix);
+  uint32_t* s_local = s_rel + kMaxRadix;
   uint32_t* s_wsum = s_local + kMaxRadix;
   uint8_t* s_map = reinterpret_cast<uint8_t*>(s_wsum + 32);
 
@@ -212,35 +123,34 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // byte-aligned 8-bit digit: one PRMT picks it out of the right 32-bit word
   const uint32_t byte_sel = 0x4440u | uint32_t((shift & 31) >> 3);
   const bool hi_word = shift >= 32;
+  const uint32_t smem_base = smem_u32(smem_raw);
 
   if (tid == 0) {
-    // ticket 0 is the scan chaser (when enabled); tiles are tickets 1..
-    const uint32_t t = atomicAdd(P.tile_counter, 1u) - (OS_CHASER ? 1u : 0u);
+    const uint32_t t = atomicAdd(P.tile_counter, 1u);
     s_tile = t;
-    // warm L2 with a tile that a block starting a few microseconds from now
-    // will claim; its TMA then hits L2 instead of waiting on HBM
-    const uint32_t pf = t + P.prefetch_tiles;
-    if (t != 0xffffffffu && P.prefetch_tiles != 0 && pf + 1 < P.num_tiles) {
-      const size_t off = size_t(pf) * P.tile_keys;
-      const K* pk = static_cast<const K*>(P.src_keys) + off;
-      if ((reinterpret_cast<uintptr_t>(pk) & 15u) == 0 && ((P.tile_keys * sizeof(K)) & 15u) == 0)
-        l2_prefetch(pk, P.tile_keys * sizeof(K));
-      if (HAS_V) {
-        const VS* pv = static_cast<const VS*>(P.src_vals) + off;
-        if ((reinterpret_cast<uintptr_t>(pv) & 15u) == 0 && ((P.tile_keys * sizeof(VS)) & 15u) == 0)
-          l2_prefetch(pv, P.tile_keys * sizeof(VS));
-      }
-    }
     s_fast = -1;
     s_reads = s_waits = s_rounds = 0;
     mbar_init(&s_bar_k, 1);
     mbar_init(&s_bar_v, 1);
     fence_mbar_init();
+    // warm L2 with a tile that a block starting a few microseconds from now
+    // will claim; its TMA then hits L2 instead of waiting on HBM
+    const uint32_t pf = t + P.prefetch_tiles;
+    if (P.prefetch_tiles != 0 && pf + 1 < P.num_tiles) {
+      const size_t off = size_t(pf) * P.tile_keys;
+      const K* pk = static_cast<const K*>(P.src_keys) + off;
+      if ((reinterpret_cast<uintptr_t>(pk) & 15u) == 0 && ((P.tile_keys * KB) & 15u) == 0)
+        l2_prefetch(pk, P.tile_keys * KB);
+      if (HAS_V) {
+        const VS* pv = static_cast<const VS*>(P.src_vals) + off;
+        if ((reinterpret_cast<uintptr_t>(pv) & 15u) == 0 && ((P.tile_keys * VB) & 15u) == 0)
+          l2_prefetch(pv, P.tile_keys * VB);
+      }
+    }
   }
   {
     uint4* z = reinterpret_cast<uint4*>(s_whist);
-#pragma unroll
-    for (int i = tid; i < WARPS * kMaxRadix / 4; i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < int(Smem::kHist / 16); i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
   }
   if (MAPPED) {
     for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
@@ -248,20 +158,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   __syncthreads();
 
   const uint32_t tile = s_tile;
-  if constexpr (OS_CHASER && THREADS / 2 >= kMaxRadix) {
-    if (tile == 0xffffffffu) {
-      scan_chaser<THREADS>(P);
-      return;
-    }
-  }
   const uint32_t tile_start = tile * P.tile_keys;
-  unsigned long long* trace = P.trace ? P.trace + size_t(tile) * kTraceWords : nullptr;
-  if (trace && tid == 0) { trace[0] = global_ns(); trace[6] = smid(); }
   const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
   const bool full = valid == uint32_t(TILE);
-  auto status_index = [&](uint32_t t, int d) -> size_t { return status_word(t, d, radix); };
   const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
   const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
+  unsigned long long* trace = P.trace ? P.trace + size_t(tile) * kTraceWords : nullptr;
+  if (trace && tid == 0) {
+    trace[0] = global_ns();
+    trace[6] = smid();
+  }
 
   // ---- 2. TMA bulk stage ----------------------------------------------------
   const bool tma_k = ((reinterpret_cast<uintptr_t>(gk) & 15u) == 0) &&
@@ -282,9 +188,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // Warp-striped ownership: warp w owns tile positions [w*ITEMS*32, (w+1)*ITEMS*32),
   // item i / lane l is position w*ITEMS*32 + i*32 + l.  Ranking walks items in
-  // that order, so ranks are stable (binning.py:71-76).  Keys stay in the
-  // shared tile buffer while they are ranked (registers hold only the packed
-  // ranks); ragged or misaligned tiles are first copied there by the threads.
+  // that order, so ranks are stable (binning.py:71-76).  Ragged or misaligned
+  // tiles are copied by the threads that will rank them (no barrier needed).
   const uint32_t warp_base = uint32_t(warp) * (ITEMS * 32);
   if (!tma_k) {
 #pragma unroll
@@ -303,11 +208,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (tma_k) mbar_wait_parity(&s_bar_k, 0);
   if (trace && tid == 0) trace[1] = global_ns();
 
-  auto load_key = [&](uint32_t idx) -> K {
-    const K x = s_keys[idx];
-    return CODED ? cin(x) : x;
-  };
-  auto digit = [&](K x) -> uint32_t {
+  auto digit = [&](K x) -> uint32_t {  // x is an encoded key
     uint32_t d;
     if (BYTE) {
       uint32_t w;
@@ -324,52 +225,42 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   };
 
   // ---- 3. warp-level multisplit ranking -------------------------------------
-  // Positions past `valid` (ragged last tile) take the largest digit: they sit
-  // after every real key, so they never perturb a real key's rank, and their
-  // count is removed from the top digit before publishing.
-  uint32_t ranks[(ITEMS + 1) / 2];  // two u16 ranks per register
+  // Counters and ranks are 16-bit, pre-scaled by the key width and inclusive
+  // (the key's own slot is counted): the highest peer stores its rank as the
+  // digit's new running count, and warp offset + rank - KB is the byte offset
+  // of the key's slot.  Positions past `valid` (ragged last tile) take the
+  // largest digit: they sit after every real key, so they never perturb a
+  // real key's rank, and their count is removed from the top digit before
+  // publishing.
+  K keys[ITEMS];                    // encoded keys, kept for the reorder
+  uint32_t ranks[(ITEMS + 1) / 2];  // two u16 scaled ranks per register
+  const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
   auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
-    uint32_t* my_hist = s_whist + warp * kMaxRadix;
-    const uint32_t hbase = smem_u32(my_hist);
-    (void)hbase;
-    (void)my_hist;
     const uint32_t lt = lanemask_lt();
     const uint32_t le = lt | (1u << lane);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
+      const K x = CODED ? cin(s_keys[idx]) : s_keys[idx];
+      if (OS_KEYS_IN_REGS) keys[i] = x;
       uint32_t d;
       if (FULL)
-        d = digit(load_key(idx));
+        d = digit(x);
       else
-        d = idx < valid ? digit(load_key(idx)) : uint32_t(radix - 1);
-#if OS_RANK_V2
-      // inclusive rank (own slot counted); the highest peer stores it as the
-      // digit's new running count
+        d = idx < valid ? digit(x) : uint32_t(radix - 1);
       uint32_t upto;
       bool leader;
       match_rank8(d, le, ~le, &upto, &leader);
-      const uint32_t caddr = hbase + d * 4u;
-      const uint32_t rank = lds_u32(caddr) + __popc(upto);
+      const uint32_t caddr = hbase + d * 2u;
+      const uint32_t rank = lds_u16(caddr) + __popc(upto) * KB;
       if (i & 1)
         ranks[i / 2] = __byte_perm(ranks[i / 2], rank, 0x5410);
       else
         ranks[i / 2] = rank;
       __syncwarp();
-      if (leader) sts_u32(caddr, rank);
+      if (leader) sts_u16(caddr, rank);
       __syncwarp();
-#else
-      const uint32_t peers = match_peers8(d);
-      const uint32_t rank = my_hist[d] + __popc(peers & lt);
-      if (i & 1)
-        ranks[i / 2] += rank << 16;
-      else
-        ranks[i / 2] = rank;
-      __syncwarp();
-      if (peers <= le) my_hist[d] = rank + 1;  // highest peer: count after this batch
-      __syncwarp();
-#endif
     }
   };
   if (full)
@@ -384,9 +275,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     uint32_t sum = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
-    if (tid == radix - 1) sum -= uint32_t(TILE) - valid;
-    count = sum;
-    st_relaxed_gpu(P.status + status_index(tile, tid), (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    count = sum / KB;
+    if (tid == radix - 1) count -= uint32_t(TILE) - valid;
+    st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
+                   (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
   if (trace && tid == 0) trace[2] = global_ns();
@@ -402,25 +294,30 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   uint32_t local_start = 0;
   if (tid < radix) {
     uint32_t wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+#pragma unroll
+    for (int w = 0; w < kMaxRadix / 32; ++w) wpre += (w < warp) ? s_wsum[w] : 0u;
     local_start = wpre + incl - count;
     s_local[tid] = local_start;
-    // fold the tile-local start into every warp's exclusive offset so the
-    // reorder needs a single shared-memory gather per key
-    uint32_t run = local_start - (OS_RANK_V2 ? 1u : 0u);  // ranks are inclusive in V2
+    // fold the tile-local start into every warp's counter, so the reorder
+    // needs a single shared-memory gather per key
+    uint32_t run = local_start * KB;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const uint32_t c = s_whist[w * kMaxRadix + tid];
-      s_whist[w * kMaxRadix + tid] = run;
+      s_whist[w * kMaxRadix + tid] = uint16_t(run);
       run += c;
     }
   }
-  // pull this thread's keys (and values) into registers; after the barrier
-  // the tile buffers are rewritten in place as per-digit runs
-  K keys[ITEMS];
-  VS vals[HAS_V ? ITEMS : 1];
+  // keys and values into registers; after the barrier the tile buffers are
+  // rewritten in place as per-digit runs
+  if (!OS_KEYS_IN_REGS) {
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) keys[i] = load_key(warp_base + i * 32 + lane);
+    for (int i = 0; i < ITEMS; ++i) {
+      const K x = s_keys[warp_base + i * 32 + lane];
+      keys[i] = CODED ? cin(x) : x;
+    }
+  }
+  VS vals[HAS_V ? ITEMS : 1];
   if (HAS_V) {
     if (tma_v) mbar_wait_parity(&s_bar_v, 0);
 #pragma unroll
@@ -432,16 +329,21 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // ---- 5a. local reorder into per-digit runs (needs no global offsets, so it
   // runs before the look-back and gives predecessors time to publish) ---------
   if (fast < 0) {
-    const uint32_t* my_off = s_whist + warp * kMaxRadix;
+    const uint32_t slot0 = smem_base - KB;  // inclusive ranks start at KB
     auto stage = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
-        const uint32_t rank = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
-        const uint32_t slot = my_off[digit(keys[i])] + rank;
-        s_keys[slot] = keys[i];
-        if (HAS_V) s_vals[slot] = vals[i];
+        const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
+        const uint32_t addr = slot0 + lds_u16(hbase + digit(keys[i]) * 2u) + r;
+        sts_val(addr, keys[i]);
+        if (HAS_V) {
+          constexpr int kSh = log2i(KB);
+          constexpr int vSh = log2i(VB > 0 ? VB : 1);
+          const uint32_t slot = (addr - smem_base) >> kSh;
+          sts_val(smem_base + uint32_t(Smem::kKeys) + (slot << vSh), vals[i]);
+        }
       }
     };
     if (full)
@@ -452,56 +354,13 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   if (trace && tid == 0) trace[3] = global_ns();
   // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
-  // A new tile starts every ~30 ns while a status round trip through L2 takes
-  // ~0.5-1 us, so the most recent G is typically 15-30 tiles back: each round
-  // trip therefore reads kLookbackWindow predecessor words at once (one
-  // look-back instead of several when the window was 4).  Then publish G and
-  // the per-digit output bases.
+  // kLookbackWindow predecessor words per round trip; stop at the first G,
+  // re-poll a predecessor that has not published yet.  Then publish G and the
+  // per-digit output indices.
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
-    if (tile > 0 && OS_LB_VEC) {
-      // groups of four predecessors, OS_LB_GROUPS 16-byte loads per round trip
-      const uint32_t* col = P.status + size_t(tid) * 4;
-      const size_t gstride = size_t(radix) * 4;
-      int j = int(tile) - 1;  // next predecessor to add
-      bool done = false;
-      while (!done) {
-        const int g = j >> 2;
-        uint4 w[OS_LB_GROUPS];
-#pragma unroll
-        for (int k = 0; k < OS_LB_GROUPS; ++k)
-          w[k] = g - k >= 0 ? ld_relaxed_gpu_v4(col + size_t(g - k) * gstride)
-                            : make_uint4(kFlagGlobal, kFlagGlobal, kFlagGlobal, kFlagGlobal);
-        reads += 4 * OS_LB_GROUPS;
-        ++rounds;
-        int next = (g - OS_LB_GROUPS + 1) * 4 - 1;
-        bool stop = false;
-#pragma unroll
-        for (int k = 0; k < OS_LB_GROUPS; ++k) {
-          const uint32_t w4[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
-#pragma unroll
-          for (int e = 3; e >= 0; --e) {
-            const int pos = (g - k) * 4 + e;
-            if (!stop && pos <= j) {
-              const uint32_t x = w4[e];
-              if (x & kFlagLocal) {
-                excl += x & kValueMask;
-              } else if (x & kFlagGlobal) {
-                excl += x & kValueMask;
-                stop = done = true;
-              } else {  // predecessor in flight: re-poll from it
-                stop = true;
-                next = pos;
-                ++waits;
-              }
-            }
-          }
-        }
-        j = next;
-      }
-      st_relaxed_gpu(P.status + status_index(tile, tid), kFlagGlobal | (excl + count));
-    } else if (tile > 0) {
+    if (tile > 0) {
       const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
       bool done = false;
@@ -528,13 +387,13 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         }
         j -= k;
       }
-      st_relaxed_gpu(P.status + status_index(tile, tid), kFlagGlobal | (excl + count));
+      st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
     if (trace && tid == 0) trace[4] = global_ns();
     const unsigned long long gbase = P.base_offsets[tid] + excl;
     const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
-    s_kptr[tid] = reinterpret_cast<unsigned long long>(P.dst_keys) + rel * sizeof(K);
-    if (HAS_V) s_vptr[tid] = reinterpret_cast<unsigned long long>(P.dst_vals) + rel * sizeof(VS);
+    s_ptr[tid] = rel;
+    s_rel[tid] = uint32_t(rel);
     if (P.carry_out != nullptr && tile == P.num_tiles - 1) P.carry_out[tid] = gbase + count;
     if (P.tile_status != nullptr)  // final word in the reference's CounterMatrix format
       P.tile_status[size_t(tile) * radix + tid] = kFlagGlobal | (excl + count);
@@ -546,25 +405,27 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   }
   __syncthreads();
 
+  K* const dst_k = static_cast<K*>(P.dst_keys);
+  VS* const dst_v = static_cast<VS*>(P.dst_vals);
   if (fast >= 0) {
     // ---- short circuit: homogeneous tile is one contiguous run --------------
-    K* out_k = reinterpret_cast<K*>(s_kptr[fast]);  // local start is 0
-    VS* out_v = HAS_V ? reinterpret_cast<VS*>(s_vptr[fast]) : nullptr;
+    const unsigned long long base = s_ptr[fast];  // local start is 0
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
-        out_k[idx] = CODED ? cout(keys[i]) : keys[i];
-        if (HAS_V) out_v[idx] = vals[i];
+        st_global(dst_k + base + idx, CODED ? cout(keys[i]) : keys[i]);
+        if (HAS_V) st_global(dst_v + base + idx, vals[i]);
       }
     }
-  } else {
-    // ---- 5b. coalesced run writes: slot s of digit d lands at kptr[d] + s ----
+  } else if (!P.wide_index) {
+    // ---- 5b. coalesced run writes: slot s of digit d lands at rel[d] + s ----
+    // (output indices below 2^32: one 32-bit table entry per digit)
     auto write_slot = [&](uint32_t s) {
       const K x = s_keys[s];
-      const uint32_t d = digit(x);
-      st_global(reinterpret_cast<K*>(s_kptr[d]) + s, CODED ? cout(x) : x);
-      if (HAS_V) st_global(reinterpret_cast<VS*>(s_vptr[d]) + s, s_vals[s]);
+      const uint32_t at = s_rel[digit(x)] + s;
+      st_global(dst_k + at, CODED ? cout(x) : x);
+      if (HAS_V) st_global(dst_v + at, s_vals[s]);
     };
     if (full) {
 #pragma unroll
@@ -572,9 +433,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     } else {
       for (uint32_t s = tid; s < valid; s += THREADS) write_slot(s);
     }
+  } else {
+    for (uint32_t s = tid; s < valid; s += THREADS) {
+      const K x = s_keys[s];
+      const unsigned long long at = s_ptr[digit(x)] + s;
+      st_global(dst_k + at, CODED ? cout(x) : x);
+      if (HAS_V) st_global(dst_v + at, s_vals[s]);
+    }
   }
-
   if (trace && tid == 0) trace[5] = global_ns();
+
   if (P.stats != nullptr && tid == 0) {
     if (fast >= 0) atomicAdd(&P.stats[0], 1ull);
     atomicAdd(&P.stats[1], (unsigned long long)s_reads);
@@ -599,21 +467,23 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     configured = true;
   }
   if (p.num_tiles == 0) return cudaSuccess;
-  kern<<<p.num_tiles + (OS_CHASER ? 1 : 0), THREADS, Smem::kBytes, stream>>>(p);
+  kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
   return cudaGetLastError();
 }
 
-// Tile geometry per (key, value) width.  THREADS x ITEMS keys per tile; the
-// shared-memory footprint decides how many tiles an SM keeps in flight.
+// Tile geometry per (key, value) width: THREADS x ITEMS keys per tile, MINB
+// resident blocks per SM.  Small blocks with many keys per thread keep four
+// tiles per SM in flight, which hides the TMA and look-back latencies of
+// each (measured in profiles/round1_binning_notes.md).
 template <int KB, int VB> struct Geometry;
-#ifndef OS_U32_MINB
-#define OS_U32_MINB 4
-#endif
 #ifndef OS_U32_THREADS
 #define OS_U32_THREADS 256
 #endif
 #ifndef OS_U32_ITEMS
 #define OS_U32_ITEMS 32
+#endif
+#ifndef OS_U32_MINB
+#define OS_U32_MINB 4
 #endif
 template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
@@ -680,7 +550,8 @@ int binning_tile_capacity(int key_bytes, int val_bytes) {
   return 0;
 }
 
-// Status words of one strip (look-back layout, see the kernel).
+// Status words of one strip: [tile][digit], the reference's CounterMatrix
+// layout (lookback.py:63-79), padded to a multiple of four tiles.
 size_t status_words_for(size_t tiles, int radix) { return (tiles + 3) / 4 * 4 * size_t(radix); }
 
 }  // namespace osb

@@ -130,6 +130,14 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
 template <typename T>
 __device__ __forceinline__ void sts_val(uint32_t addr, T v) {
   if constexpr (sizeof(T) == 8)
@@ -295,6 +303,7 @@ struct PassParams {
   const uint8_t* digit_map;                // [2^map_bits] -> destination, or null
   uint32_t prefetch_tiles;                 // L2-prefetch distance in tiles (0: off)
   unsigned long long* trace;               // diagnostics: kTraceWords per tile, or null
+  uint32_t wide_index;                     // output indices may reach 2^32 (64-bit run writes)
 };
 // Per-tile trace record (globaltimer ns): claim, keys staged, L published,
 // reorder done, warp 0 G published, warp 0 done, SM id, unused.
