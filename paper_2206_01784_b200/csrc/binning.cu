@@ -62,6 +62,26 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #define OS_KEYS_IN_REGS 0
 #endif
 
+// 1: the first look-back window is loaded before the reorder and consumed
+// after it, so its round trip overlaps the reorder.
+#ifndef OS_EARLY_LOOKBACK
+#define OS_EARLY_LOOKBACK 0
+#endif
+
+// Per-tile timeline records (os_debug_trace) are compiled in only for
+// diagnostic builds (-DOS_TRACE=1); the product kernel carries no trace code.
+#ifndef OS_TRACE
+#define OS_TRACE 0
+#endif
+// The ranking loop orders each item's counter read before the leader's
+// counter write, and that write before the next item's read.  The accesses
+// are volatile, so they keep program order, and the warp is converged (no
+// divergent branches in the loop), so they also execute in order.
+// OS_SYNCWARP=1 adds the formal __syncwarp() fences (two NOPs per item).
+#ifndef OS_SYNCWARP
+#define OS_SYNCWARP 1
+#endif
+
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
 
 template <int THREADS, int ITEMS, int KB, int VB>
@@ -163,8 +183,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const bool full = valid == uint32_t(TILE);
   const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
   const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
-  unsigned long long* trace = P.trace ? P.trace + size_t(tile) * kTraceWords : nullptr;
-  if (trace && tid == 0) {
+  unsigned long long* trace =
+      (OS_TRACE && P.trace) ? P.trace + size_t(tile) * kTraceWords : nullptr;
+  if (OS_TRACE && trace && tid == 0) {
     trace[0] = global_ns();
     trace[6] = smid();
   }
@@ -206,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   }
   if (tma_k) mbar_wait_parity(&s_bar_k, 0);
-  if (trace && tid == 0) trace[1] = global_ns();
+  if (OS_TRACE && trace && tid == 0) trace[1] = global_ns();
 
   auto digit = [&](K x) -> uint32_t {  // x is an encoded key
     uint32_t d;
@@ -258,9 +279,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         ranks[i / 2] = __byte_perm(ranks[i / 2], rank, 0x5410);
       else
         ranks[i / 2] = rank;
-      __syncwarp();
+      if (OS_SYNCWARP) __syncwarp();
       if (leader) sts_u16(caddr, rank);
-      __syncwarp();
+      if (OS_SYNCWARP) __syncwarp();
     }
   };
   if (full)
@@ -281,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
                    (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
-  if (trace && tid == 0) trace[2] = global_ns();
+  if (OS_TRACE && trace && tid == 0) trace[2] = global_ns();
   // block-wide exclusive scan of counts over digits (first 8 warps)
   uint32_t incl = count;
 #pragma unroll
@@ -323,6 +344,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
   }
+  // first look-back window, in flight during the reorder (OS_EARLY_LOOKBACK)
+  uint32_t lbw[kLookbackWindow];
+  if (OS_EARLY_LOOKBACK && tid < radix && tile > 0) {
+#pragma unroll
+    for (int k = 0; k < kLookbackWindow; ++k)
+      lbw[k] = (int(tile) - 1 - k >= 0)
+                   ? ld_relaxed_gpu(P.status + size_t(int(tile) - 1 - k) * radix + tid)
+                   : kFlagGlobal;
+  }
   __syncthreads();
   const int fast = s_fast;
 
@@ -352,7 +382,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       stage(std::false_type{});
   }
 
-  if (trace && tid == 0) trace[3] = global_ns();
+  if (OS_TRACE && trace && tid == 0) trace[3] = global_ns();
   // ---- 4b. decoupled look-back (lookback.py:144-169) ------------------------
   // kLookbackWindow predecessor words per round trip; stop at the first G,
   // re-poll a predecessor that has not published yet.  Then publish G and the
@@ -364,11 +394,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
       bool done = false;
+      bool first = true;
       while (!done) {
         uint32_t w[kLookbackWindow];
 #pragma unroll
         for (int k = 0; k < kLookbackWindow; ++k)
-          w[k] = (j - k >= 0) ? ld_relaxed_gpu(col + size_t(j - k) * radix) : kFlagGlobal;
+          w[k] = (OS_EARLY_LOOKBACK && first) ? lbw[k]
+                 : (j - k >= 0)               ? ld_relaxed_gpu(col + size_t(j - k) * radix)
+                                              : kFlagGlobal;
+        first = false;
         reads += kLookbackWindow;
         ++rounds;
         int k = 0;
@@ -389,7 +423,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       }
       st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
-    if (trace && tid == 0) trace[4] = global_ns();
+    if (OS_TRACE && trace && tid == 0) trace[4] = global_ns();
     const unsigned long long gbase = P.base_offsets[tid] + excl;
     const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
     s_ptr[tid] = rel;
@@ -441,7 +475,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (HAS_V) st_global(dst_v + at, s_vals[s]);
     }
   }
-  if (trace && tid == 0) trace[5] = global_ns();
+  if (OS_TRACE && trace && tid == 0) trace[5] = global_ns();
 
   if (P.stats != nullptr && tid == 0) {
     if (fast >= 0) atomicAdd(&P.stats[0], 1ull);

@@ -27,4 +27,4 @@ for pf in 0 296; do
   ONESWEEP_B200_PREFETCH=$pf timeout 300 python bench.py --steps 20 --warmup 5 --e2e-steps 0 --no-cpu-baseline > gpurun_out/pf_${TAG}_$pf.json 2>/dev/null
   python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print('prefetch', sys.argv[2], round(d['value'],2), [round(x) for x in d['kernels']['binning_pass_us']])" gpurun_out/pf_${TAG}_$pf.json $pf
 done
-timeout 300 python tools/lookback_diag.py; timeout 300 python tools/trace_diag.py 1
+timeout 300 python tools/lookback_diag.py; ONESWEEP_B200_LIB=$PWD/paper_2206_01784_b200/_lib/variants/trace.so timeout 300 python tools/trace_diag.py 1
