@@ -522,12 +522,22 @@ template <int KB, int VB> struct Geometry;
 template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
-template <> struct Geometry<4, 4> { static constexpr int T = 512, I = 16, B = 2; };
+#ifndef OS_P32_T
+#define OS_P32_T 512
+#define OS_P32_I 16
+#define OS_P32_B 2
+#endif
+#ifndef OS_K64_T
+#define OS_K64_T 256  // tools/bench_configs.py: 1687 us/pass vs 2045 with 512 x 8
+#define OS_K64_I 16
+#define OS_K64_B 3
+#endif
+template <> struct Geometry<4, 4> { static constexpr int T = OS_P32_T, I = OS_P32_I, B = OS_P32_B; };
 template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; };
 template <> struct Geometry<8, 0> { static constexpr int T = 512, I = 8, B = 2; };
 template <> struct Geometry<8, 1> { static constexpr int T = 512, I = 8, B = 2; };
 template <> struct Geometry<8, 2> { static constexpr int T = 512, I = 8, B = 2; };
-template <> struct Geometry<8, 4> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<8, 4> { static constexpr int T = OS_K64_T, I = OS_K64_I, B = OS_K64_B; };
 template <> struct Geometry<8, 8> { static constexpr int T = 512, I = 8, B = 2; };
 
 template <typename K, typename V>
