@@ -17,4 +17,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:binn
   python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_bin_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:histogram -s 1 -c 1 -f -o gpurun_out/prof_hist_$TAG \
   python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_hist_$TAG.log 2>&1
+
+timeout 900 python tools/bench_configs.py --steps 5 > gpurun_out/cfgs_$TAG.jsonl 2>&1
 echo done
