@@ -82,6 +82,10 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #define OS_SYNCWARP 1
 #endif
 
+#ifndef OS_FMA_ADDS
+#define OS_FMA_ADDS 0
+#endif
+
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
 
 template <int THREADS, int ITEMS, int KB, int VB>
@@ -144,6 +148,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const uint32_t byte_sel = 0x4440u | uint32_t((shift & 31) >> 3);
   const bool hi_word = shift >= 32;
   const uint32_t smem_base = smem_u32(smem_raw);
+  // opaque small constants for FMA-pipe integer arithmetic (see fma_u32);
+  // OS_FMA_ADDS=0 leaves the adds to the compiler (ALU-pipe IADD3/LEA)
+  const uint32_t k_one = OS_FMA_ADDS ? opaque_all_ones() >> 31 : 1u;
+  const uint32_t k_two = k_one + k_one;
+  const uint32_t k_shl16 = k_one << 16;
 
   if (tid == 0) {
     const uint32_t t = atomicAdd(P.tile_counter, 1u);
@@ -273,10 +282,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       uint32_t upto;
       bool leader;
       match_rank8(d, le, ~le, &upto, &leader);
-      const uint32_t caddr = hbase + d * 2u;
+      const uint32_t caddr = fma_u32(d, k_two, hbase);
       const uint32_t rank = lds_u16(caddr) + __popc(upto) * KB;
       if (i & 1)
-        ranks[i / 2] = __byte_perm(ranks[i / 2], rank, 0x5410);
+        ranks[i / 2] = fma_u32(rank, k_shl16, ranks[i / 2]);
       else
         ranks[i / 2] = rank;
       if (OS_SYNCWARP) __syncwarp();
@@ -366,7 +375,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       for (int i = 0; i < ITEMS; ++i) {
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
         const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
-        const uint32_t addr = slot0 + lds_u16(hbase + digit(keys[i]) * 2u) + r;
+        const uint32_t off = lds_u16(fma_u32(digit(keys[i]), k_two, hbase));
+        const uint32_t addr = fma_u32(off, k_one, fma_u32(r, k_one, slot0));
         sts_val(addr, keys[i]);
         if (HAS_V) {
           constexpr int kSh = log2i(KB);
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     // (output indices below 2^32: one 32-bit table entry per digit)
     auto write_slot = [&](uint32_t s) {
       const K x = s_keys[s];
-      const uint32_t at = s_rel[digit(x)] + s;
+      const uint32_t at = fma_u32(s_rel[digit(x)], k_one, s);
       st_global(dst_k + at, CODED ? cout(x) : x);
       if (HAS_V) st_global(dst_v + at, s_vals[s]);
     };

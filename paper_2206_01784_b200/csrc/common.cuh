@@ -77,8 +77,39 @@ struct XorCodec {
 // clear, and the eight masks folded with three-input LOP3s.  __match_any_sync
 // computes the same mask but issues on the ADU pipe, which capped the first
 // kernel at ~14% of HBM bandwidth (profiles/round1_binning_v1.md).
+#ifndef OS_NOT_ON_FMA
+#define OS_NOT_ON_FMA 1
+#endif
+// 0xffffffff that ptxas cannot constant-fold (lanemask_lt | lanemask_ge), so
+// x * m + m stays an IMAD instead of being rewritten as an ALU-pipe IADD3.
+__device__ __forceinline__ uint32_t opaque_all_ones() {
+  uint32_t a, b;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(a));
+  asm("mov.u32 %0, %%lanemask_ge;" : "=r"(b));
+  return a | b;
+}
+// Integer a*m + c forced onto the FMA pipe (IMAD).  The ranking and reorder
+// loops are limited by the ALU pipe (LOP3/PRMT/VOTE issue at half rate), so
+// adds and small multiplies go to the otherwise idle FMA pipe.  `m` should be
+// an opaque register value (e.g. opaque_all_ones() >> 31 for 1).
+__device__ __forceinline__ uint32_t fma_u32(uint32_t a, uint32_t m, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(m), "r"(c));
+  return r;
+}
 __device__ __forceinline__ uint32_t vote_bit(uint32_t d, uint32_t bit) {
   uint32_t m;  // ballot of "bit set", complemented by the lanes whose bit is clear
+#if OS_NOT_ON_FMA
+  // ~x == x * (-1) + (-1): the complement issues on the FMA pipe (IMAD), not
+  // the ALU pipe that the ballots and LOP3 folds already saturate
+  asm("{\n\t.reg .pred p;\n\t"
+      "and.b32 %0, %1, %2;\n\t"
+      "setp.ne.u32 p, %0, 0;\n\t"
+      "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+      "@!p mad.lo.u32 %0, %0, %3, %3;\n\t}"
+      : "=r"(m)
+      : "r"(d), "r"(bit), "r"(opaque_all_ones()));
+#else
   asm("{\n\t.reg .pred p;\n\t"
       "and.b32 %0, %1, %2;\n\t"
       "setp.ne.u32 p, %0, 0;\n\t"
@@ -86,6 +117,7 @@ __device__ __forceinline__ uint32_t vote_bit(uint32_t d, uint32_t bit) {
       "@!p not.b32 %0, %0;\n\t}"
       : "=r"(m)
       : "r"(d), "r"(bit));
+#endif
   return m;
 }
 __device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
