@@ -301,10 +301,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
+  uint32_t wc[WARPS];  // this digit's per-warp counts, kept for the offsets below
   if (tid < radix) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
+    for (int w = 0; w < WARPS; ++w) {
+      wc[w] = s_whist[w * kMaxRadix + tid];
+      sum += wc[w];
+    }
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
     st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
@@ -333,9 +337,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     uint32_t run = local_start * KB;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
-      const uint32_t c = s_whist[w * kMaxRadix + tid];
       s_whist[w * kMaxRadix + tid] = uint16_t(run);
-      run += c;
+      run += wc[w];
     }
   }
   // keys and values into registers; after the barrier the tile buffers are
