@@ -536,8 +536,8 @@ template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I =
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
 #ifndef OS_P32_T
-#define OS_P32_T 512
-#define OS_P32_I 16
+#define OS_P32_T 256  // tools/bench_configs.py: 1212 us/pass at q=1 vs 1245 with 512 x 16
+#define OS_P32_I 32
 #define OS_P32_B 2
 #endif
 #ifndef OS_K64_T
