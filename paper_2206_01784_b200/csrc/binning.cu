@@ -82,6 +82,10 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #define OS_SYNCWARP 1
 #endif
 
+// Skip the multisplit for warps whose 32*ITEMS keys share one digit.
+#ifndef OS_UNIFORM_WARPS
+#define OS_UNIFORM_WARPS 1
+#endif
 #ifndef OS_FMA_ADDS
 #define OS_FMA_ADDS 0
 #endif
@@ -293,10 +297,41 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (OS_SYNCWARP) __syncwarp();
     }
   };
-  if (full)
-    rank_items(std::true_type{});
-  else
-    rank_items(std::false_type{});
+  // A warp whose keys all carry one digit needs no multisplit: its inclusive
+  // ranks are the positions themselves.  Test cheaply first (first and last
+  // item), then every item; uniform keys fail the first test at once, while
+  // low-entropy and presorted inputs skip the ballots for most warps.
+  // (key-value passes only: in the 64-register keys-only kernel the extra
+  // code spills and costs the uniform-key case 2.6 %)
+  bool uniform_warp = false;
+  if (OS_UNIFORM_WARPS && HAS_V && full) {
+    const K xa = CODED ? cin(s_keys[warp_base + lane]) : s_keys[warp_base + lane];
+    const K xb = CODED ? cin(s_keys[warp_base + (ITEMS - 1) * 32 + lane])
+                       : s_keys[warp_base + (ITEMS - 1) * 32 + lane];
+    const uint32_t d0 = __shfl_sync(0xffffffffu, digit(xa), 0);
+    if (__all_sync(0xffffffffu, digit(xa) == d0 && digit(xb) == d0)) {
+      bool same = true;
+#pragma unroll
+      for (int i = 1; i < ITEMS - 1; ++i) {
+        const K x = CODED ? cin(s_keys[warp_base + i * 32 + lane]) : s_keys[warp_base + i * 32 + lane];
+        same &= digit(x) == d0;
+      }
+      uniform_warp = __all_sync(0xffffffffu, same);
+      if (uniform_warp) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; i += 2)
+          ranks[i / 2] = uint32_t(i * 32 + lane + 1) * KB |
+                         (i + 1 < ITEMS ? uint32_t((i + 1) * 32 + lane + 1) * KB << 16 : 0u);
+        if (lane == 0) sts_u16(hbase + d0 * 2u, uint32_t(ITEMS * 32 * KB));
+      }
+    }
+  }
+  if (!uniform_warp) {
+    if (full)
+      rank_items(std::true_type{});
+    else
+      rank_items(std::false_type{});
+  }
   __syncthreads();
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
