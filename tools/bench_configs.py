@@ -94,6 +94,8 @@ def main():
         cfgs.append((f"C4 {str(dt).split('.')[1]} keys + u32 values", lambda dt=dt: (
             generate_keys(KeyGenSpec(q=1, seed=0, n=n, key_bits=64), device=dev).view(dt),
             torch.arange(n, dtype=torch.int32, device=dev).view(torch.uint32), dt)))
+    cfgs.append(("C5 single-GPU 2^31 u32 keys (8 strips)", lambda: (
+        generate_keys(KeyGenSpec(q=1, seed=0, n=1 << 31), device=dev), None, torch.uint32)))
     for name, make in cfgs:
         if a.only and a.only not in name:
             continue
