@@ -86,6 +86,11 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #ifndef OS_UNIFORM_WARPS
 #define OS_UNIFORM_WARPS 1
 #endif
+// 1: keys-only u32 passes park each thread's keys in TMEM between ranking and
+// the reorder (no shared-memory re-read, fewer live registers).
+#ifndef OS_TMEM_STASH
+#define OS_TMEM_STASH 1
+#endif
 #ifndef OS_FMA_ADDS
 #define OS_FMA_ADDS 0
 #endif
@@ -122,6 +127,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   static_assert(32 * ITEMS * KB < 65536, "u16 scaled per-warp counters");
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
   constexpr int VB = HAS_V ? int(sizeof(VS)) : 0;
+  // TMEM key stash: warp w owns lanes 32*(w%4).., columns (w/4)*ITEMS..
+  constexpr bool STASH = OS_TMEM_STASH && KB == 4 && !HAS_V && ITEMS % 8 == 0 && WARPS % 4 == 0;
+  constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * ITEMS;
+  constexpr uint32_t TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
+                           : TCOLS_RAW <= 256 ? 256 : 512;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -139,6 +149,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   __shared__ uint32_t s_reads, s_waits, s_rounds;
   __shared__ __align__(8) uint64_t s_bar_k;
   __shared__ __align__(8) uint64_t s_bar_v;
+  __shared__ uint32_t s_tmem;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -158,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const uint32_t k_two = k_one + k_one;
   const uint32_t k_shl16 = k_one << 16;
 
+  if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
   if (tid == 0) {
     const uint32_t t = atomicAdd(P.tile_counter, 1u);
     s_tile = t;
@@ -188,7 +200,13 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (MAPPED) {
     for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
   }
+  if (STASH) tmem_fence_before_sync();
   __syncthreads();
+  uint32_t taddr = 0;
+  if (STASH) {
+    tmem_fence_after_sync();
+    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * ITEMS;
+  }
 
   const uint32_t tile = s_tile;
   const uint32_t tile_start = tile * P.tile_keys;
@@ -266,7 +284,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // largest digit: they sit after every real key, so they never perturb a
   // real key's rank, and their count is removed from the top digit before
   // publishing.
-  K keys[ITEMS];                    // encoded keys, kept for the reorder
+  K keys[STASH ? 1 : ITEMS];        // encoded keys, kept for the reorder
+  uint32_t kc[8];                   // TMEM stash chunk
   uint32_t ranks[(ITEMS + 1) / 2];  // two u16 scaled ranks per register
   const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
   auto rank_items = [&](auto full_tag) {
@@ -277,7 +296,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       const K x = CODED ? cin(s_keys[idx]) : s_keys[idx];
-      if (OS_KEYS_IN_REGS) keys[i] = x;
+      if constexpr (OS_KEYS_IN_REGS && !STASH) keys[i] = x;
+      if (STASH) {
+        kc[i & 7] = uint32_t(x);
+        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(i - 7), kc);
+      }
       uint32_t d;
       if (FULL)
         d = digit(x);
@@ -332,6 +355,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     else
       rank_items(std::false_type{});
   }
+  if (STASH) tmem_wait_st();
   __syncthreads();
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
@@ -378,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   }
   // keys and values into registers; after the barrier the tile buffers are
   // rewritten in place as per-digit runs
-  if (!OS_KEYS_IN_REGS) {
+  if constexpr (!OS_KEYS_IN_REGS && !STASH) {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const K x = s_keys[warp_base + i * 32 + lane];
@@ -411,11 +435,13 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
+        if (STASH && (i & 7) == 0) tmem_ld8(taddr + uint32_t(i), kc);
+        const K key = STASH ? K(kc[i & 7]) : keys[STASH ? 0 : i];
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
         const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
-        const uint32_t off = lds_u16(fma_u32(digit(keys[i]), k_two, hbase));
+        const uint32_t off = lds_u16(fma_u32(digit(key), k_two, hbase));
         const uint32_t addr = fma_u32(off, k_one, fma_u32(r, k_one, slot0));
-        sts_val(addr, keys[i]);
+        sts_val(addr, key);
         if (HAS_V) {
           constexpr int kSh = log2i(KB);
           constexpr int vSh = log2i(VB > 0 ? VB : 1);
@@ -485,7 +511,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       atomicAdd(&s_rounds, rounds);
     }
   }
+  if (STASH) tmem_fence_before_sync();
   __syncthreads();
+  if (STASH && warp == 0) {
+    tmem_fence_after_sync();
+    tmem_dealloc(s_tmem, TCOLS);
+  }
 
   K* const dst_k = static_cast<K*>(P.dst_keys);
   VS* const dst_v = static_cast<VS*>(P.dst_vals);
@@ -496,7 +527,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
-        st_global(dst_k + base + idx, CODED ? cout(keys[i]) : keys[i]);
+        const K key = STASH ? (CODED ? cin(s_keys[idx]) : s_keys[idx]) : keys[STASH ? 0 : i];
+        st_global(dst_k + base + idx, CODED ? cout(key) : key);
         if (HAS_V) st_global(dst_v + base + idx, vals[i]);
       }
     }
@@ -562,10 +594,10 @@ template <int KB, int VB> struct Geometry;
 #define OS_U32_THREADS 256
 #endif
 #ifndef OS_U32_ITEMS
-#define OS_U32_ITEMS 32
+#define OS_U32_ITEMS 64
 #endif
 #ifndef OS_U32_MINB
-#define OS_U32_MINB 4
+#define OS_U32_MINB 3
 #endif
 template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB; };
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
