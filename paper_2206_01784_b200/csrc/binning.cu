@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (tid == 0) {
     if (tma_k) {
       mbar_arrive_expect_tx(&s_bar_k, valid * sizeof(K));
-      tma_bulk_g2s(s_keys, gk, valid * sizeof(K), &s_bar_k);
+      tma_bulk_g2s_hint(s_keys, gk, valid * sizeof(K), &s_bar_k, l2_policy_evict_first());
     }
     if (HAS_V && tma_v) {
       mbar_arrive_expect_tx(&s_bar_v, valid * sizeof(VS));
@@ -360,14 +360,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
-  uint32_t wc[WARPS];  // this digit's per-warp counts, kept for the offsets below
   if (tid < radix) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
-      wc[w] = s_whist[w * kMaxRadix + tid];
-      sum += wc[w];
-    }
+    for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
     st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
@@ -395,9 +391,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     // needs a single shared-memory gather per key
     uint32_t run = local_start * KB;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
+    for (int w = 0; w < WARPS; ++w) {  // counts re-read: registers are scarce here
+      const uint32_t c = s_whist[w * kMaxRadix + tid];
       s_whist[w * kMaxRadix + tid] = uint16_t(run);
-      run += wc[w];
+      run += c;
     }
   }
   // keys and values into registers; after the barrier the tile buffers are
@@ -538,7 +535,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     auto write_slot = [&](uint32_t s) {
       const K x = s_keys[s];
       const uint32_t at = fma_u32(s_rel[digit(x)], k_one, s);
-      st_global(dst_k + at, CODED ? cout(x) : x);
+      if constexpr (sizeof(K) == 4)
+        st_global_cs(reinterpret_cast<uint32_t*>(dst_k + at), uint32_t(CODED ? cout(x) : x));
+      else
+        st_global(dst_k + at, CODED ? cout(x) : x);
       if (HAS_V) st_global(dst_v + at, s_vals[s]);
     };
     if (full) {

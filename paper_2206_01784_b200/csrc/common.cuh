@@ -233,6 +233,18 @@ __device__ __forceinline__ void st_global(T* p, T v) {
     asm volatile("st.global.b8 [%0], %1;" ::"l"(p), "r"((uint32_t)v) : "memory");
 }
 
+// Run-write store: streaming (.cs), the output of a pass is not re-read by
+// this pass, and tile loads carry an L2 evict_first policy, so the status
+// words and prefetched tiles keep their L2 lines (~1 % per pass,
+// profiles/round1_binning_notes.md).
+__device__ __forceinline__ void st_global_cs(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -358,6 +370,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                  "+r"(v[6]), "+r"(v[7])
                :
                : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s_hint(void* dst_smem, const void* src_gmem,
+                                                  uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 // ---- launch descriptors ------------------------------------------------------
