@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
   constexpr int VB = HAS_V ? int(sizeof(VS)) : 0;
   // TMEM key stash: warp w owns lanes 32*(w%4).., columns (w/4)*ITEMS..
-  constexpr bool STASH = OS_TMEM_STASH && KB == 4 && !HAS_V && ITEMS % 8 == 0 && WARPS % 4 == 0;
-  constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * ITEMS;
+  constexpr bool STASH = OS_TMEM_STASH && KB == 4 && (!HAS_V || VB == 4) && ITEMS % 8 == 0 &&
+                         WARPS % 4 == 0;
+  constexpr int NW = HAS_V ? 2 : 1;  // stashed words per item: key (+ value)
+  constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * ITEMS * NW;
   constexpr uint32_t TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                            : TCOLS_RAW <= 256 ? 256 : 512;
 
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   uint32_t taddr = 0;
   if (STASH) {
     tmem_fence_after_sync();
-    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * ITEMS;
+    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * (ITEMS * NW);
   }
 
   const uint32_t tile = s_tile;
@@ -285,7 +287,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // real key's rank, and their count is removed from the top digit before
   // publishing.
   K keys[STASH ? 1 : ITEMS];        // encoded keys, kept for the reorder
-  uint32_t kc[8];                   // TMEM stash chunk
+  uint32_t kc[8];                   // TMEM stash chunk (keys)
+  uint32_t vc[8];                   // TMEM stash chunk (values)
   uint32_t ranks[(ITEMS + 1) / 2];  // two u16 scaled ranks per register
   const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
   auto rank_items = [&](auto full_tag) {
@@ -346,6 +349,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           ranks[i / 2] = uint32_t(i * 32 + lane + 1) * KB |
                          (i + 1 < ITEMS ? uint32_t((i + 1) * 32 + lane + 1) * KB << 16 : 0u);
         if (lane == 0) sts_u16(hbase + d0 * 2u, uint32_t(ITEMS * 32 * KB));
+        if constexpr (STASH) {  // the keys still go to the stash
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) {
+            const K x = s_keys[warp_base + i * 32 + lane];
+            kc[i & 7] = uint32_t(CODED ? cin(x) : x);
+            if ((i & 7) == 7) tmem_st8(taddr + uint32_t(i - 7), kc);
+          }
+        }
       }
     }
   }
@@ -406,11 +417,20 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       keys[i] = CODED ? cin(x) : x;
     }
   }
-  VS vals[HAS_V ? ITEMS : 1];
+  VS vals[HAS_V && !STASH ? ITEMS : 1];
   if (HAS_V) {
     if (tma_v) mbar_wait_parity(&s_bar_v, 0);
+    if constexpr (STASH) {  // values to the stash, next to the keys
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
+      for (int i = 0; i < ITEMS; ++i) {
+        kc[i & 7] = uint32_t(s_vals[warp_base + i * 32 + lane]);
+        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(ITEMS + i - 7), kc);
+      }
+      tmem_wait_st();
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
+    }
   }
   // first look-back window, in flight during the reorder (OS_EARLY_LOOKBACK)
   uint32_t lbw[kLookbackWindow];
@@ -433,6 +453,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         if (STASH && (i & 7) == 0) tmem_ld8(taddr + uint32_t(i), kc);
+        if (STASH && HAS_V && (i & 7) == 0) tmem_ld8(taddr + uint32_t(ITEMS + i), vc);
         const K key = STASH ? K(kc[i & 7]) : keys[STASH ? 0 : i];
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
         const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
@@ -443,7 +464,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           constexpr int kSh = log2i(KB);
           constexpr int vSh = log2i(VB > 0 ? VB : 1);
           const uint32_t slot = (addr - smem_base) >> kSh;
-          sts_val(smem_base + uint32_t(Smem::kKeys) + (slot << vSh), vals[i]);
+          sts_val(smem_base + uint32_t(Smem::kKeys) + (slot << vSh),
+                  STASH ? VS(vc[i & 7]) : vals[STASH ? 0 : i]);
         }
       }
     };
@@ -526,7 +548,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (idx < valid) {
         const K key = STASH ? (CODED ? cin(s_keys[idx]) : s_keys[idx]) : keys[STASH ? 0 : i];
         st_global(dst_k + base + idx, CODED ? cout(key) : key);
-        if (HAS_V) st_global(dst_v + base + idx, vals[i]);
+        if (HAS_V) st_global(dst_v + base + idx, STASH ? s_vals[idx] : vals[STASH ? 0 : i]);
       }
     }
   } else if (!P.wide_index) {
@@ -605,7 +627,7 @@ template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2;
 #ifndef OS_P32_T
 #define OS_P32_T 256  // tools/bench_configs.py: 1212 us/pass at q=1 vs 1245 with 512 x 16
 #define OS_P32_I 32
-#define OS_P32_B 2
+#define OS_P32_B 3
 #endif
 #ifndef OS_K64_T
 #define OS_K64_T 256  // tools/bench_configs.py: 1687 us/pass vs 2045 with 512 x 8
