@@ -178,6 +178,20 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in,
                      const unsigned long long* seg_offsets, void* workspace,
                      size_t workspace_bytes, void* stream);
 
+/* Fused partition + exchange over peer memory (NVLink): like
+ * os_msd_partition, but dest_index is a device u64[parts] of element indices,
+ * relative to keys_out / vals_out, where this rank's segment starts in each
+ * destination's receive buffer (two's-complement differences when the buffer
+ * is a peer-mapped allocation).  Replaces the partition + all-to-all pair of
+ * the NCCL path.  Values need val_bytes == key_bytes and peer
+ * value buffers at the same element distance from vals_out as the key
+ * buffers from keys_out (one symmetric allocation per rank). */
+int os_msd_partition_p2p(const void* keys_in, void* keys_out, const void* vals_in,
+                         void* vals_out, size_t n, int key_type, int val_bytes,
+                         int digit_bits, int end_bit, const unsigned int* bin_lo, int parts,
+                         const unsigned long long* dest_index, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

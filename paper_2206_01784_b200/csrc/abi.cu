@@ -594,4 +594,49 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in, v
                   s, /*dense_bases=*/true);
 }
 
+// Fused partition + exchange: the same stable partition, but segment g is
+// written straight into destination g's receive buffer.  dest_index[g] is the
+// element index, relative to keys_out (and vals_out), at which this rank's
+// segment starts on destination g -- a two's-complement difference when
+// keys_out and the peer buffer are different (peer-mapped) allocations.  With
+// values, peer value buffers must sit at the same element distance from
+// vals_out as the key buffers from keys_out (one symmetric allocation per
+// rank, key_bytes == val_bytes).
+int os_msd_partition_p2p(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                         size_t n, int key_type, int val_bytes, int digit_bits, int end_bit,
+                         const unsigned int* bin_lo, int parts,
+                         const unsigned long long* dest_index, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (val_bytes != 0 && val_bytes != kt.bytes)
+    return fail(OS_ERR_ARG, "p2p exchange with values needs val_bytes == key_bytes");
+  if ((val_bytes == 0) != (vals_in == nullptr) || (val_bytes == 0) != (vals_out == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  if (int rc = check_bits(kt.bytes, digit_bits, end_bit - digit_bits, end_bit)) return rc;
+  if (parts < 1 || parts > kMaxRadix) return fail(OS_ERR_ARG, "parts must be in [1, 256]");
+  if (n == 0) return OS_OK;
+  uint32_t tile;
+  if (int rc = resolve_tile(0, kt.bytes, val_bytes, &tile)) return rc;
+  Tiling t = make_tiling(n, tile, kMaxStripKeys);
+  PassWs w = pass_ws(t, parts, true);
+  const size_t need = align_up(kMaxRadix) + w.bytes;
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(OS_ERR_WORKSPACE, "msd workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  uint8_t* map = ws;
+  unsigned char* pws = ws + align_up(kMaxRadix);
+  OS_CUDA(cudaMemsetAsync(pws, 0, w.zero_bytes, s), "msd memset");
+  build_digit_map<<<1, kMaxRadix, 0, s>>>(bin_lo, parts, 1 << digit_bits, map);
+  OS_CUDA(cudaGetLastError(), "digit map");
+  unsigned long long* carry_final =
+      reinterpret_cast<unsigned long long*>(pws + w.off_carry) + (t.strips - 1) * size_t(parts);
+  // dense_bases=false: 64-bit output indices, so the peer offsets wrap correctly
+  return run_pass(keys_in, keys_out, vals_in, vals_out, kt.bytes, val_bytes, t,
+                  end_bit - digit_bits, digit_bits, parts, map, dest_index, carry_final, kt.enc,
+                  kt.dec, reinterpret_cast<uint32_t*>(pws + w.off_status), nullptr, pws, w, nullptr,
+                  s, /*dense_bases=*/false);
+}
+
 }  // extern "C"

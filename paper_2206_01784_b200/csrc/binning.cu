@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       const uint32_t idx = warp_base + i * 32 + lane;
       if (idx < valid) {
         const K key = STASH ? (CODED ? cin(s_keys[idx]) : s_keys[idx]) : keys[STASH ? 0 : i];
-        st_global(dst_k + base + idx, CODED ? cout(key) : key);
-        if (HAS_V) st_global(dst_v + base + idx, STASH ? s_vals[idx] : vals[STASH ? 0 : i]);
+        st_global(elem_at(dst_k, base + idx), CODED ? cout(key) : key);
+        if (HAS_V) st_global(elem_at(dst_v, base + idx), STASH ? s_vals[idx] : vals[STASH ? 0 : i]);
       }
     }
   } else if (!P.wide_index) {
@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (uint32_t s = tid; s < valid; s += THREADS) {
       const K x = s_keys[s];
       const unsigned long long at = s_ptr[digit(x)] + s;
-      st_global(dst_k + at, CODED ? cout(x) : x);
-      if (HAS_V) st_global(dst_v + at, s_vals[s]);
+      st_global(elem_at(dst_k, at), CODED ? cout(x) : x);
+      if (HAS_V) st_global(elem_at(dst_v, at), s_vals[s]);
     }
   }
   if (OS_TRACE && trace && tid == 0) trace[5] = global_ns();

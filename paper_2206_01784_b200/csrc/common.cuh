@@ -245,6 +245,13 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// base + index for 64-bit output indices that may be "negative" (two's
+// complement): os_msd_partition_p2p addresses peer receive buffers relative to
+// the local output base, so the index wraps modulo 2^64 by design.
+template <typename T>
+__device__ __forceinline__ T* elem_at(T* base, unsigned long long index) {
+  return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(base) + index * sizeof(T));
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

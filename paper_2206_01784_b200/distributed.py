@@ -22,8 +22,15 @@ concatenating the outputs in rank order equals the stable sort of the
 concatenated inputs.  Whole-bin splitting balances uniform keys; under heavy
 skew one destination receives the largest bin.
 
-The exchange uses device tensors with NCCL; with any other backend (gloo in
-the CPU tests) it is staged through host memory.
+Exchange backends:
+* "p2p" (NCCL groups whose ranks share an NVLink domain): steps 4 and 5 fuse.
+  Every rank holds one symmetric receive buffer (torch symmetric memory, peer
+  mapped), and os_msd_partition_p2p writes each destination's segment straight
+  into that destination's buffer at its final offset, so the exchange is the
+  partition pass's own stores over NVLink followed by one barrier;
+* "nccl": partition into a local send buffer, then all_to_all_single;
+* any other backend (gloo in the CPU tests) stages the all-to-all through host
+  memory.
 """
 
 from __future__ import annotations
@@ -55,6 +62,29 @@ def plan_split(table: np.ndarray, parts: int) -> list[int]:
         bounds.append(max(k, bounds[-1]))
     bounds.append(radix)
     return bounds
+
+
+def receive_offsets(table: np.ndarray, bin_lo: list[int], rank: int) -> list[int]:
+    """Where `rank`'s segment for destination g starts in g's receive buffer:
+    sources are concatenated in rank order (the global input order), so it is
+    the count that lower ranks send to g."""
+    table = np.asarray(table, dtype=np.uint64)
+    parts = len(bin_lo) - 1
+    return [int(table[:rank, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(parts)]
+
+
+def p2p_dest_index(peer_ptrs: list[int], local_ptr: int, elem_bytes: int,
+                   recv_off: list[int]) -> np.ndarray:
+    """u64 element indices, relative to this rank's receive buffer `local_ptr`,
+    of its segment starts in every destination's (peer-mapped) receive buffer.
+    Differences wrap modulo 2^64; the kernel adds them in 64-bit arithmetic."""
+    out = []
+    for g, ptr in enumerate(peer_ptrs):
+        delta = int(ptr) - int(local_ptr)
+        if delta % elem_bytes:
+            raise ValueError("peer buffers must be aligned to the element size")
+        out.append((delta // elem_bytes + int(recv_off[g])) % (1 << 64))
+    return np.array(out, dtype=np.uint64)
 
 
 def exchange_counts(table: np.ndarray, bin_lo: list[int], rank: int) -> tuple[list[int], list[int]]:
@@ -102,6 +132,27 @@ class DeviceOps:
         )
         return out_k, out_v
 
+    def partition_p2p(self, keys, values, spec, digit_bits: int, bin_lo: list[int],
+                      dest_index: np.ndarray, recv_k, recv_v):
+        """Stable partition whose segment g lands at element dest_index[g]
+        relative to recv_k (recv_v): straight into peer receive buffers."""
+        import torch
+
+        dev = keys.device
+        parts = len(bin_lo) - 1
+        lo = torch.tensor(bin_lo, dtype=torch.int32, device=dev)
+        idx = torch.from_numpy(dest_index.view(np.int64).copy()).to(dev)
+        L = _native.load()
+        ws = workspace(L.os_msd_partition_workspace_bytes(keys.numel()), dev)
+        vb = 0 if values is None else values.element_size()
+        _native.check(
+            L.os_msd_partition_p2p(_native.ptr(keys), _native.ptr(recv_k), _native.ptr(values),
+                                   _native.ptr(recv_v), keys.numel(), spec.type_id, vb, digit_bits,
+                                   spec.bits, _native.ptr(lo), parts, _native.ptr(idx),
+                                   _native.ptr(ws), ws.numel(), _native.stream_handle()),
+            "msd_partition_p2p",
+        )
+
     def local_sort(self, keys, values):
         from .binning import onesweep_sort
 
@@ -125,11 +176,67 @@ def _all_to_all(t, send: list[int], recv: list[int], group):
     return out.view(t.dtype)
 
 
+class SymmetricReceive:
+    """One peer-mapped receive buffer per rank (torch symmetric memory):
+    keys at [0, cap), values at [cap, 2 cap) elements of the key width, the
+    same layout on every rank, so one element index reaches a peer's key and
+    value slot alike (os_msd_partition_p2p)."""
+
+    def __init__(self, cap: int, elem_bytes: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.cap, self.elem_bytes = cap, elem_bytes
+        name = (group or dist.group.WORLD).group_name
+        self.buf = symm_mem.empty(2 * cap * elem_bytes, dtype=torch.uint8, device=device)
+        self.handle = symm_mem.rendezvous(self.buf, name)
+        self.peer_ptrs = [int(p) for p in self.handle.buffer_ptrs]
+
+    def views(self, dtype, vdtype=None):
+        eb = self.elem_bytes
+        k = self.buf[: self.cap * eb].view(dtype)
+        v = self.buf[self.cap * eb:].view(vdtype) if vdtype is not None else None
+        return k, v
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
+_SYMM = {}
+
+
+def _symmetric_receive(need: int, elem_bytes: int, device, group):
+    key = (id(group), elem_bytes, str(device))
+    cur = _SYMM.get(key)
+    if cur is None or cur.cap < need:
+        cur = _SYMM[key] = SymmetricReceive(max(need, 1), elem_bytes, device, group)
+    return cur
+
+
+def _p2p_usable(keys, values, group) -> bool:
+    import torch.distributed as dist
+
+    if dist.get_backend(group) != "nccl" or not keys.is_cuda:
+        return False
+    if values is not None and values.element_size() != keys.element_size():
+        return False
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except ImportError:
+        return False
+    return True
+
+
 def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = SPLIT_DIGIT_BITS,
-                 return_plan: bool = False):
+                 return_plan: bool = False, exchange: str = "auto"):
     """Stable sort of the global array whose rank-order concatenation is
     `keys` over all ranks of `group`.  Returns this rank's contiguous slice
-    of the sorted output (and values)."""
+    of the sorted output (and values).
+
+    exchange: "p2p" (fused partition + peer stores), "nccl"/"staged"
+    (partition + all_to_all_single), or "auto" (p2p when the group is NCCL and
+    symmetric memory is available, else all-to-all)."""
     import torch
     import torch.distributed as dist
 
@@ -151,14 +258,68 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     bin_lo = plan_split(table, world)
     send, recv = exchange_counts(table, bin_lo, rank)
 
-    part_k, part_v = ops.partition(keys, values, spec, digit_bits, bin_lo, send)
-    recv_k = _all_to_all(part_k, send, recv, group)
-    recv_v = _all_to_all(part_v, send, recv, group) if values is not None else None
+    if exchange == "auto":
+        exchange = "p2p" if _p2p_usable(keys, values, group) else "all_to_all"
+    if exchange == "p2p":
+        # capacity: the largest receive count of any rank (same on all ranks)
+        need = max(int(table[:, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(world))
+        rb = _symmetric_receive(need, keys.element_size(), keys.device, group)
+        rk, rv = rb.views(keys.dtype, None if values is None else values.dtype)
+        rb.barrier()  # every receiver is done with the previous round's data
+        dest = p2p_dest_index(rb.peer_ptrs, rb.peer_ptrs[rank], keys.element_size(),
+                              receive_offsets(table, bin_lo, rank))
+        ops.partition_p2p(keys, values, spec, digit_bits, bin_lo, dest, rk, rv)
+        rb.barrier()  # all peers' stores into this rank's buffer have landed
+        total = sum(recv)
+        recv_k = rk[:total]
+        recv_v = rv[:total] if values is not None else None
+    else:
+        part_k, part_v = ops.partition(keys, values, spec, digit_bits, bin_lo, send)
+        recv_k = _all_to_all(part_k, send, recv, group)
+        recv_v = _all_to_all(part_v, send, recv, group) if values is not None else None
     out_k, out_v = ops.local_sort(recv_k, recv_v)
     result = out_k if values is None else (out_k, out_v)
     if return_plan:
-        return result, {"bin_lo": bin_lo, "send": send, "recv": recv}
+        return result, {"bin_lo": bin_lo, "send": send, "recv": recv, "exchange": exchange}
     return result
+
+
+def emulate_p2p_sort(shards, value_shards=None, *, ops=None, digit_bits: int = SPLIT_DIGIT_BITS):
+    """The p2p sharded sort with G logical ranks in one process on one device:
+    the same plan, receive offsets and os_msd_partition_p2p calls, with the G
+    receive buffers as separate device allocations (so the destination
+    indices are true cross-allocation differences).  Test and single-GPU
+    validation path for the fused exchange."""
+    import torch
+
+    ops = ops or DeviceOps()
+    world = len(shards)
+    spec = spec_for_dtype(shards[0].dtype)
+    eb = shards[0].element_size()
+    if value_shards is not None and any(v.element_size() != eb for v in value_shards):
+        raise ValueError("p2p exchange with values needs value width == key width")
+    hists = [ops.top_histogram(k, spec, digit_bits).view(torch.int64).cpu() for k in shards]
+    table = torch.stack(hists).numpy().view(np.uint64)
+    bin_lo = plan_split(table, world)
+    recv = [int(table[:, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(world)]
+    cap = max(max(recv), 1)
+    bufs = [torch.empty(2 * cap * eb, dtype=torch.uint8, device=shards[0].device) for _ in range(world)]
+    ptrs = [b.data_ptr() for b in bufs]
+    views = [(b[: cap * eb].view(shards[0].dtype),
+              b[cap * eb:].view(value_shards[0].dtype) if value_shards is not None else None)
+             for b in bufs]
+    for r, k in enumerate(shards):
+        dest = p2p_dest_index(ptrs, ptrs[r], eb, receive_offsets(table, bin_lo, r))
+        v = value_shards[r] if value_shards is not None else None
+        ops.partition_p2p(k, v, spec, digit_bits, bin_lo, dest, views[r][0], views[r][1])
+    torch.cuda.synchronize()
+    out = []
+    for g in range(world):
+        rk = views[g][0][: recv[g]]
+        rv = views[g][1][: recv[g]] if value_shards is not None else None
+        ok, ov = ops.local_sort(rk, rv)
+        out.append(ok if value_shards is None else (ok, ov))
+    return out, {"bin_lo": bin_lo, "recv": recv}
 
 
 class ShardedSorter:

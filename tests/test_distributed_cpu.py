@@ -142,3 +142,34 @@ def test_plan_split_properties():
     lo = plan_split(skew, 2)
     s0, _ = exchange_counts(skew, lo, 0)
     assert sorted(s0) == [0, 100]
+
+
+def test_p2p_receive_offsets_and_dest_index():
+    """Host logic of the fused exchange: source segments are concatenated in
+    rank order at each destination, and the u64 destination index reaches the
+    peer slot from the local base modulo 2^64 (peer below or above)."""
+    from paper_2206_01784_b200.distributed import (exchange_counts, p2p_dest_index, plan_split,
+                                                   receive_offsets)
+
+    rng = np.random.default_rng(7)
+    world = 4
+    table = rng.integers(0, 1000, size=(world, 256)).astype(np.uint64)
+    bin_lo = plan_split(table, world)
+    for rank in range(world):
+        off = receive_offsets(table, bin_lo, rank)
+        send, _ = exchange_counts(table, bin_lo, rank)
+        for g in range(world):
+            # this rank's segment ends where the next source's begins
+            nxt = receive_offsets(table, bin_lo, rank + 1)[g] if rank + 1 < world else None
+            if nxt is not None:
+                assert off[g] + send[g] == nxt
+        assert off == [int(table[:rank, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(world)]
+    ptrs = [0x7F0000000000, 0x7E0000001000, 0x7F8000000200, 0x100]
+    for eb in (4, 8):
+        for rank in range(world):
+            off = receive_offsets(table, bin_lo, rank)
+            idx = p2p_dest_index(ptrs, ptrs[rank], eb, off)
+            for g in range(world):
+                assert (ptrs[rank] + int(idx[g]) * eb) % (1 << 64) == ptrs[g] + off[g] * eb
+    with pytest.raises(ValueError):
+        p2p_dest_index([0x1000, 0x1002], 0x1000, 4, [0, 0])

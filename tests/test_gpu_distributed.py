@@ -91,3 +91,82 @@ def test_msd_partition_is_stable_segmentation(cuda):
     order = np.argsort(dest, kind="stable")
     assert np.array_equal(pk.cpu().numpy(), keys[order])
     assert np.array_equal(pv.cpu().numpy(), vals[order])
+
+
+def _p2p_case(world, dtype, sizes, q=1, with_values=True, seed=11):
+    from oracle import oracle
+    from paper_2206_01784_b200.distributed import emulate_p2p_sort
+
+    rng = np.random.default_rng(seed)
+    bits = np.dtype(dtype).itemsize * 8
+    shards = []
+    for n in sizes:
+        raw = np.full(n, (1 << bits) - 1, dtype=np.uint64)
+        for _ in range(q):  # AND of q words: the keygen's entropy reduction
+            raw &= rng.integers(0, 2**bits, size=n, dtype=np.uint64)
+        shards.append((raw.astype(np.uint32) if bits == 32 else raw).view(dtype))
+    vdt = np.uint32 if bits == 32 else np.uint64
+    vals, start = [], 0
+    for s in shards:
+        vals.append(np.arange(start, start + s.size, dtype=vdt))
+        start += s.size
+    tk = [torch.from_numpy(s).cuda() for s in shards]
+    tv = [torch.from_numpy(v).cuda() for v in vals] if with_values else None
+    out, plan = emulate_p2p_sort(tk, tv)
+    if with_values:
+        got_k = np.concatenate([o[0].cpu().numpy() for o in out])
+        got_v = np.concatenate([o[1].cpu().numpy() for o in out])
+    else:
+        got_k = np.concatenate([o.cpu().numpy() for o in out])
+    want_k, want_v = oracle.sharded_sort(shards, vals)
+    u = np.uint32 if bits == 32 else np.uint64
+    assert np.array_equal(got_k.view(u), want_k.view(u))
+    if with_values:
+        assert np.array_equal(got_v.astype(np.uint64), want_v.astype(np.uint64))
+    # each rank's slice is what the plan said it would receive
+    lens = [(o[0] if with_values else o).numel() for o in out]
+    assert lens == plan["recv"]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_p2p_exchange_u32_pairs(cuda, world):
+    """Fused partition + peer stores (os_msd_partition_p2p) into separate
+    per-rank receive allocations: the destination indices are real
+    cross-allocation pointer differences, as with peer-mapped NVLink buffers."""
+    rng = np.random.default_rng(world)
+    sizes = [int(rng.integers(100_000, 300_000)) for _ in range(world)]
+    _p2p_case(world, np.uint32, sizes)
+
+
+@pytest.mark.parametrize("dtype,q", [(np.int32, 1), (np.float32, 1), (np.uint64, 1),
+                                     (np.float64, 1), (np.uint32, 16)])
+def test_p2p_exchange_key_types_and_skew(cuda, dtype, q):
+    _p2p_case(3, dtype, [200_001, 150_000, 99_999], q=q)
+
+
+def test_p2p_exchange_keys_only_and_empty_shard(cuda):
+    _p2p_case(3, np.uint32, [250_000, 0, 123_457], with_values=False)
+
+
+def test_p2p_exchange_all_equal_keys_one_destination(cuda):
+    """All keys in one top-digit bin: one rank receives everything, the
+    others nothing (whole-bin splitting), and stability still holds."""
+    from oracle import oracle
+    from paper_2206_01784_b200.distributed import emulate_p2p_sort
+
+    shards = [np.full(n, 0xABACADAE, dtype=np.uint32) for n in (70_000, 90_000)]
+    vals = [np.arange(70_000, dtype=np.uint32), np.arange(70_000, 160_000, dtype=np.uint32)]
+    out, plan = emulate_p2p_sort([torch.from_numpy(s).cuda() for s in shards],
+                                 [torch.from_numpy(v).cuda() for v in vals])
+    assert sorted(plan["recv"]) == [0, 160_000]
+    got_v = np.concatenate([o[1].cpu().numpy() for o in out])
+    assert np.array_equal(got_v, oracle.sharded_sort(shards, vals)[1])
+
+
+def test_p2p_rejects_mixed_widths(cuda):
+    from paper_2206_01784_b200.distributed import emulate_p2p_sort
+
+    k = torch.zeros(1000, dtype=torch.uint32, device="cuda")
+    v = torch.zeros(1000, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        emulate_p2p_sort([k, k], [v, v])
