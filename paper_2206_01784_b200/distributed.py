@@ -214,10 +214,13 @@ def _symmetric_receive(need: int, elem_bytes: int, device, group):
     return cur
 
 
+_P2P_BROKEN = False
+
+
 def _p2p_usable(keys, values, group) -> bool:
     import torch.distributed as dist
 
-    if dist.get_backend(group) != "nccl" or not keys.is_cuda:
+    if _P2P_BROKEN or dist.get_backend(group) != "nccl" or not keys.is_cuda:
         return False
     if values is not None and values.element_size() != keys.element_size():
         return False
@@ -258,12 +261,22 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     bin_lo = plan_split(table, world)
     send, recv = exchange_counts(table, bin_lo, rank)
 
-    if exchange == "auto":
-        exchange = "p2p" if _p2p_usable(keys, values, group) else "all_to_all"
-    if exchange == "p2p":
+    rb = None
+    if exchange in ("auto", "p2p") and (exchange == "p2p" or _p2p_usable(keys, values, group)):
         # capacity: the largest receive count of any rank (same on all ranks)
         need = max(int(table[:, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(world))
-        rb = _symmetric_receive(need, keys.element_size(), keys.device, group)
+        try:
+            rb = _symmetric_receive(need, keys.element_size(), keys.device, group)
+        except Exception as e:  # no symmetric memory on this system: all-to-all
+            if exchange == "p2p":
+                raise
+            global _P2P_BROKEN
+            _P2P_BROKEN = True
+            import warnings
+
+            warnings.warn(f"p2p exchange unavailable ({e}); using all_to_all")
+    exchange = "p2p" if rb is not None else "all_to_all"
+    if rb is not None:
         rk, rv = rb.views(keys.dtype, None if values is None else values.dtype)
         rb.barrier()  # every receiver is done with the previous round's data
         dest = p2p_dest_index(rb.peer_ptrs, rb.peer_ptrs[rank], keys.element_size(),
