@@ -41,9 +41,19 @@ struct HistCounter {
   XorCodec<K> codec;
 
   __device__ __forceinline__ void add_place(K x, int p, uint32_t m) const {
-    const uint32_t d = digit_of(x, begin + p * dbits, m);
+    uint32_t d;
+    if constexpr (FIXED_PASSES == 8 && sizeof(K) == 8) {
+      // eight 8-bit places over a 64-bit key: place p is byte p (one PRMT)
+      const uint32_t w = p < 4 ? uint32_t(uint64_t(x)) : uint32_t(uint64_t(x) >> 32);
+      d = __byte_perm(w, 0u, 0x4440u + uint32_t(p & 3));
+    } else {
+      d = digit_of(x, begin + p * dbits, m);
+    }
     const uint32_t word = (uint32_t(p * half_radix) + (d >> 1)) * 32u;
-    atomicAdd(lane_base + word, 1u << ((d & 1u) << 4));
+    // no return value needed: a reduction, not an atomic exchange
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(lane_base + word)),
+                 "r"(1u << ((d & 1u) << 4))
+                 : "memory");
   }
   __device__ __forceinline__ void add(K x) const {
     x = codec(x);
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
 #pragma unroll
     for (int u = 0; u < kHistVec; ++u) cur[u] = nxt[u];
     v0 = v1;
-    if ((r + 1) % kRoundsPerPortion == 0) fold();
+    if ((r + 1) % (kRoundsPerPortion * (sizeof(K) == 8 ? 2 : 1)) == 0) fold();
   }
   // unaligned head / ragged tail (< 2 vectors of keys in total)
   const size_t g = size_t(blockIdx.x) * kHistThreads + tid;
