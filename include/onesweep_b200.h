@@ -178,6 +178,18 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in,
                      const unsigned long long* seg_offsets, void* workspace,
                      size_t workspace_bytes, void* stream);
 
+/* ---- reduce-then-scan ablation (rts_sort, baseline.py:121-173) ----------
+ * The reference's comparator sort on the device: per 8-bit place an upsweep
+ * (per-tile histograms, n reads), a digit-major prefix (baseline.py:76-84)
+ * and a downsweep that is the binning kernel with the look-back replaced by
+ * the prefix table (n reads + n writes).  Same output as os_sort; n < 2^32.
+ * events (optional): 3 * passes + 1 events recorded before the first
+ * upsweep and after every upsweep, prefix and downsweep. */
+size_t os_rts_sort_workspace_bytes(size_t n, int key_type, int val_bytes);
+int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
+                size_t n, int key_type, int val_bytes, void* workspace,
+                size_t workspace_bytes, void** events, int num_events, void* stream);
+
 /* Fused partition + exchange over peer memory (NVLink): like
  * os_msd_partition, but dest_index is a device u64[parts] of element indices,
  * relative to keys_out / vals_out, where this rank's segment starts in each

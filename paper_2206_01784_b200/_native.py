@@ -55,6 +55,8 @@ SIGNATURES = {
     "os_msd_partition_workspace_bytes": (_sz, [_sz]),
     "os_msd_partition": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),
     "os_msd_partition_p2p": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),
+    "os_rts_sort_workspace_bytes": (_sz, [_sz, _i, _i]),
+    "os_rts_sort": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp, _i, _vp]),
 }
 
 

@@ -639,4 +639,142 @@ int os_msd_partition_p2p(const void* keys_in, void* keys_out, const void* vals_i
                   s, /*dense_bases=*/false);
 }
 
+// ---- reduce-then-scan ablation (baseline.py:121-173) ------
+// The reference's rts_sort on the device: per digit place an upsweep (n key
+// reads), a digit-major prefix over the per-tile table, and a downsweep that
+// is the binning kernel with the look-back replaced by the table (2n), so
+// 3n element transfers per place against Onesweep's 2n.  Full-width 8-bit
+// places; the keys are encoded in the first upsweep/downsweep and decoded in
+// the last downsweep like os_sort.
+struct RtsLayout {
+  int passes = 0;
+  Tiling t;
+  PassWs pw;
+  size_t off_tmp_k = 0, off_tmp_v = 0, off_counts = 0, off_offsets = 0, off_csum = 0,
+         off_pass = 0, total = 0;
+};
+
+static RtsLayout rts_layout(size_t n, int kb, int vb, uint32_t tile) {
+  RtsLayout L;
+  L.passes = kb * 8 / 8;
+  L.t = make_tiling(n, tile, kMaxStripKeys);
+  L.pw = pass_ws(L.t, kMaxRadix, /*own_status=*/false);
+  const size_t tiles = L.t.tiles_total;
+  size_t off = 0;
+  L.off_tmp_k = off;
+  off = align_up(off + n * kb);
+  L.off_tmp_v = off;
+  off = align_up(off + n * vb);
+  L.off_counts = off;
+  off = align_up(off + tiles * kMaxRadix * 4);
+  L.off_offsets = off;
+  off = align_up(off + tiles * kMaxRadix * 8);
+  L.off_csum = off;
+  off = align_up(off + rts_chunk_count(tiles) * kMaxRadix * 8);
+  L.off_pass = off;
+  off += L.pw.bytes;
+  L.total = off;
+  return L;
+}
+
+size_t os_rts_sort_workspace_bytes(size_t n, int key_type, int val_bytes) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt) || !valid_val_bytes(val_bytes)) return 0;
+  uint32_t tile;
+  if (resolve_tile(0, kt.bytes, val_bytes, &tile)) return 0;
+  return rts_layout(n, kt.bytes, val_bytes, tile).total;
+}
+
+int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out, size_t n,
+                int key_type, int val_bytes, void* workspace, size_t workspace_bytes,
+                void** events, int num_events, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if ((val_bytes == 0) != (vals_in == nullptr) || (val_bytes == 0) != (vals_out == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int kb = kt.bytes, vb = val_bytes;
+  if (n <= 1) {  // baseline.py:151-153
+    if (n == 1) {
+      OS_CUDA(cudaMemcpyAsync(keys_out, keys_in, kb, cudaMemcpyDeviceToDevice, s), "copy");
+      if (vb) OS_CUDA(cudaMemcpyAsync(vals_out, vals_in, vb, cudaMemcpyDeviceToDevice, s), "copy");
+    }
+    return OS_OK;
+  }
+  if (n >= (size_t(1) << 32)) return fail(OS_ERR_ARG, "rts sort supports n < 2^32");
+  uint32_t tile;
+  if (int rc = resolve_tile(0, kb, vb, &tile)) return rc;
+  RtsLayout L = rts_layout(n, kb, vb, tile);
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return fail(OS_ERR_WORKSPACE, "rts workspace needs %zu bytes, got %zu", L.total, workspace_bytes);
+  if (events != nullptr && num_events < 3 * L.passes + 1)
+    return fail(OS_ERR_ARG, "need %d events, got %d", 3 * L.passes + 1, num_events);
+  auto mark = [&](int i) -> cudaError_t {
+    return events ? cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s) : cudaSuccess;
+  };
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
+  unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.off_offsets);
+  unsigned long long* csum = reinterpret_cast<unsigned long long*>(ws + L.off_csum);
+  unsigned char* pws = ws + L.off_pass;
+  void* tmp_k = ws + L.off_tmp_k;
+  void* tmp_v = ws + L.off_tmp_v;
+  const void* src_k = keys_in;
+  const void* src_v = vals_in;
+  OS_CUDA(mark(0), "event");
+  for (int k = 0; k < L.passes; ++k) {
+    const bool to_out = ((L.passes - 1 - k) % 2) == 0;
+    void* dst_k = to_out ? keys_out : tmp_k;
+    void* dst_v = to_out ? vals_out : tmp_v;
+    const int shift = 8 * k;
+    OS_CUDA(launch_rts_upsweep(src_k, n, kb, tile, shift, 0xffu, k == 0 ? kt.enc : CODEC_NONE,
+                               counts, s), "rts upsweep");
+    OS_CUDA(mark(1 + 3 * k), "event");
+    OS_CUDA(launch_rts_prefix(counts, uint32_t(L.t.tiles_total), kMaxRadix, csum, offsets, s),
+            "rts prefix");
+    OS_CUDA(mark(2 + 3 * k), "event");
+    OS_CUDA(cudaMemsetAsync(pws, 0, L.pw.zero_bytes, s), "rts memset");
+    // downsweep: the binning kernel, run starts from the table
+    uint32_t* counters = reinterpret_cast<uint32_t*>(pws + L.pw.off_counters);
+    unsigned long long* carries = reinterpret_cast<unsigned long long*>(pws + L.pw.off_carry);
+    size_t tile_base = 0;
+    for (size_t st = 0; st < L.t.strips; ++st) {
+      PassParams p{};
+      const size_t lo = st * L.t.strip;
+      p.src_keys = static_cast<const unsigned char*>(src_k) + lo * kb;
+      p.dst_keys = dst_k;
+      p.src_vals = vb ? static_cast<const unsigned char*>(src_v) + lo * vb : nullptr;
+      p.dst_vals = vb ? dst_v : nullptr;
+      p.strip_n = uint32_t(L.t.strip_len(st));
+      p.num_tiles = uint32_t(L.t.strip_tiles(st));
+      p.tile_keys = tile;
+      p.shift = shift;
+      p.mask = 0xffu;
+      p.radix = kMaxRadix;
+      const int ci_code = k == 0 ? kt.enc : CODEC_NONE, co_code = k == L.passes - 1 ? kt.dec : CODEC_NONE;
+      if (kb == 4) {
+        const auto ci = XorCodec<uint32_t>::make(ci_code), co = XorCodec<uint32_t>::make(co_code);
+        p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+      } else {
+        const auto ci = XorCodec<uint64_t>::make(ci_code), co = XorCodec<uint64_t>::make(co_code);
+        p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+      }
+      p.base_offsets = nullptr;
+      p.carry_out = carries + st * size_t(kMaxRadix);
+      p.status = nullptr;
+      p.tile_counter = counters + st;
+      p.prefetch_tiles = prefetch_tiles();
+      p.wide_index = n >= (size_t(1) << 32) - (size_t(1) << 26);
+      p.rts_offsets = offsets + tile_base * kMaxRadix;
+      OS_CUDA(launch_binning_pass(p, kb, vb, s), "rts downsweep launch");
+      tile_base += p.num_tiles;
+    }
+    OS_CUDA(mark(3 + 3 * k), "event");
+    src_k = dst_k;
+    src_v = dst_v;
+  }
+  return OS_OK;
+}
+
 }  // extern "C"

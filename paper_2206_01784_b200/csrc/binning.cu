@@ -377,8 +377,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
-    st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
-                   (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    if (P.rts_offsets == nullptr)  // (reduce-then-scan passes have no look-back)
+      st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
+                     (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
   if (OS_TRACE && trace && tid == 0) trace[2] = global_ns();
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
-    if (tile > 0) {
+    if (tile > 0 && P.rts_offsets == nullptr) {
       const uint32_t* col = P.status + tid;
       int j = int(tile) - 1;
       bool done = false;
@@ -517,7 +518,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
     if (OS_TRACE && trace && tid == 0) trace[4] = global_ns();
-    const unsigned long long gbase = P.base_offsets[tid] + excl;
+    // reduce-then-scan ablation (rts.cu): the tile's run starts come from the
+    // precomputed digit-major prefix table instead of a look-back
+    const unsigned long long gbase = P.rts_offsets != nullptr
+                                         ? P.rts_offsets[size_t(tile) * radix + tid]
+                                         : P.base_offsets[tid] + excl;
     const unsigned long long rel = gbase - local_start;  // modular: slot >= local_start
     s_ptr[tid] = rel;
     s_rel[tid] = uint32_t(rel);

@@ -412,6 +412,7 @@ struct PassParams {
   uint32_t prefetch_tiles;                 // L2-prefetch distance in tiles (0: off)
   unsigned long long* trace;               // diagnostics: kTraceWords per tile, or null
   uint32_t wide_index;                     // output indices may reach 2^32 (64-bit run writes)
+  const unsigned long long* rts_offsets;   // reduce-then-scan ablation: [num_tiles][radix] run starts, or null
 };
 // Per-tile trace record (globaltimer ns): claim, keys staged, L published,
 // reorder done, warp 0 G published, warp 0 done, SM id, unused.
@@ -452,6 +453,13 @@ cudaError_t launch_codec(const void* in, void* out, size_t n, int key_bytes, int
                          cudaStream_t stream);
 cudaError_t launch_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
                           unsigned long long first, cudaStream_t stream);
+cudaError_t launch_rts_upsweep(const void* keys, size_t n, int key_bytes, uint32_t tile_keys,
+                               int shift, uint32_t mask, int codec, uint32_t* counts,
+                               cudaStream_t stream);
+size_t rts_chunk_count(size_t tiles);
+cudaError_t launch_rts_prefix(const uint32_t* counts, uint32_t tiles, int radix,
+                              unsigned long long* csum, unsigned long long* offsets,
+                              cudaStream_t stream);
 cudaError_t launch_top_histogram(const void* keys, size_t n, int key_bytes, int codec, int shift,
                                  uint32_t mask, unsigned long long* hist, cudaStream_t stream);
 

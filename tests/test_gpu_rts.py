@@ -1,0 +1,84 @@
+"""GPU: the reduce-then-scan comparator (os_rts_sort) -- the reference's
+rts_sort contract (baseline.py:121-173, pinned by test_baseline.py:158-200)
+restated against the oracle, its 3pn ledger, and byte equality with the
+Onesweep sort at BASELINE sizes."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", [np.uint32, np.int32, np.float32, np.uint64])
+def test_rts_sort_equals_oracle(cuda, dtype):
+    from oracle import oracle
+    from paper_2206_01784_b200 import rts_sort
+
+    rng = np.random.default_rng(13)
+    bits = 64 if dtype == np.uint64 else 32
+    raw = rng.integers(0, 2**bits, size=8000, dtype=np.uint64)
+    keys = raw.astype(np.uint32).view(dtype) if bits == 32 else raw.view(dtype)
+    values = np.arange(keys.size, dtype=np.uint64)
+    got_k, got_v = rts_sort(keys, values)
+    want_k, want_v = oracle.sort(keys, values)
+    assert np.array_equal(got_k.view(np.uint8), want_k.view(np.uint8))
+    assert np.array_equal(got_v, want_v)
+
+
+def test_rts_ledger_is_3pn_and_ratio_holds(cuda):
+    from paper_2206_01784_b200 import Executor, onesweep_sort, radix_plan, rts_sort
+
+    n = 20_000
+    keys = np.random.default_rng(17).integers(0, 2**32, size=n, dtype=np.uint32)
+    cfg = radix_plan(32, 8)
+    ex_rts, ex_one = Executor(), Executor()
+    a = rts_sort(keys, cfg=cfg, executor=ex_rts)
+    b = onesweep_sort(keys, cfg=cfg, executor=ex_one)
+    assert np.array_equal(a, b)
+    rts_ops = ex_rts.ledger_snapshot().element_ops
+    one_ops = ex_one.ledger_snapshot().element_ops
+    assert rts_ops == 3 * cfg.passes * n  # 12n
+    assert one_ops == (2 * cfg.passes + 1) * n  # 9n
+
+
+def test_rts_sort_tiny_inputs(cuda):
+    from paper_2206_01784_b200 import rts_sort
+
+    assert rts_sort(np.empty(0, dtype=np.uint32)).size == 0
+    assert np.array_equal(rts_sort(np.array([7], dtype=np.uint32)), [7])
+    assert np.array_equal(rts_sort(np.array([9, 3], dtype=np.int64)), [3, 9])
+
+
+@pytest.mark.parametrize("n,q,pairs", [(1 << 24, 1, False), (12_345_679, 1, True),
+                                       (1 << 22, 16, True), (3_000_001, 4, False)])
+def test_rts_matches_onesweep_bytes(cuda, n, q, pairs):
+    from paper_2206_01784_b200 import KeyGenSpec, generate_keys, onesweep_sort, rts_sort
+
+    keys = generate_keys(KeyGenSpec(q=q, seed=n, n=n), device="cuda")
+    if pairs:
+        vals = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint32)
+        a = rts_sort(keys, vals)
+        b = onesweep_sort(keys, vals)
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    else:
+        assert torch.equal(rts_sort(keys), onesweep_sort(keys))
+
+
+def test_rts_all_equal_and_f64_pairs(cuda):
+    from oracle import oracle
+    from paper_2206_01784_b200 import rts_sort
+
+    keys = np.full(300_000, 0xABACADAE, dtype=np.uint32)
+    vals = np.arange(keys.size, dtype=np.uint32)
+    k, v = rts_sort(keys, vals)
+    assert np.array_equal(k, keys) and np.array_equal(v, vals)
+    raw = np.random.default_rng(3).integers(0, 2**64, size=200_000, dtype=np.uint64)
+    fk = raw.view(np.float64)
+    fv = np.arange(fk.size, dtype=np.uint32)
+    got = rts_sort(fk, fv)
+    want = oracle.sort(fk, fv)
+    assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))
+    assert np.array_equal(got[1], want[1])
