@@ -239,3 +239,27 @@ def test_sort_rejects_bad_arguments(cuda):
         onesweep_sort(np.zeros(4, dtype=np.uint32), cfg=radix_plan(64, 8))
     with pytest.raises(ValueError):
         onesweep_sort(np.zeros(4, dtype=np.uint32), np.zeros(3, dtype=np.uint32))
+
+
+def test_sort_pipeline_matches_onesweep_sort(cuda):
+    """SortPipeline (overlapped upload / sort / download of host batches)
+    returns, for every submitted batch, what onesweep_sort returns."""
+    import torch
+
+    from paper_2206_01784_b200 import KeyGenSpec, SortPipeline, generate_keys, onesweep_sort
+
+    n = 1_000_003
+    pipe = SortPipeline(n, torch.uint32, torch.uint32, depth=2)
+    ins, outs, want = [], [], []
+    for seed in range(5):
+        k = generate_keys(KeyGenSpec(q=1 + seed % 3, seed=seed, n=n), device="cuda").cpu().pin_memory()
+        v = torch.arange(n, dtype=torch.int32).view(torch.uint32).pin_memory()
+        ok = torch.empty(n, dtype=torch.uint32).pin_memory()
+        ov = torch.empty(n, dtype=torch.uint32).pin_memory()
+        pipe.submit(k, ok, v, ov)
+        ins.append((k, v))
+        outs.append((ok, ov))
+    pipe.synchronize()
+    for (k, v), (ok, ov) in zip(ins, outs):
+        wk, wv = onesweep_sort(k.numpy(), v.numpy())
+        assert np.array_equal(ok.numpy(), wk) and np.array_equal(ov.numpy(), wv)
