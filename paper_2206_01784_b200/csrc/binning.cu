@@ -485,17 +485,26 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
     if (tile > 0 && P.rts_offsets == nullptr) {
-      const uint32_t* col = P.status + tid;
+      // p walks down the digit's column; 8-bit places have a compile-time row
+      // stride, so the window's loads are one base register plus immediates
+      const size_t stride = BYTE ? size_t(kMaxRadix) : size_t(radix);
+      const uint32_t* p = P.status + size_t(tile - 1) * stride + tid;
       int j = int(tile) - 1;
       bool done = false;
       bool first = true;
       while (!done) {
         uint32_t w[kLookbackWindow];
+        if (OS_EARLY_LOOKBACK && first) {
 #pragma unroll
-        for (int k = 0; k < kLookbackWindow; ++k)
-          w[k] = (OS_EARLY_LOOKBACK && first) ? lbw[k]
-                 : (j - k >= 0)               ? ld_relaxed_gpu(col + size_t(j - k) * radix)
-                                              : kFlagGlobal;
+          for (int k = 0; k < kLookbackWindow; ++k) w[k] = lbw[k];
+        } else if (j >= kLookbackWindow - 1) {
+#pragma unroll
+          for (int k = 0; k < kLookbackWindow; ++k) w[k] = ld_relaxed_gpu(p - k * stride);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kLookbackWindow; ++k)
+            w[k] = (j - k >= 0) ? ld_relaxed_gpu(p - k * stride) : kFlagGlobal;
+        }
         first = false;
         reads += kLookbackWindow;
         ++rounds;
@@ -514,6 +523,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           }
         }
         j -= k;
+        p -= k * stride;
       }
       st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
