@@ -91,6 +91,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #ifndef OS_TMEM_STASH
 #define OS_TMEM_STASH 1
 #endif
+#ifndef OS_STASH64
+#define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
+#endif
 #ifndef OS_FMA_ADDS
 #define OS_FMA_ADDS 0
 #endif
@@ -128,9 +131,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
   constexpr int VB = HAS_V ? int(sizeof(VS)) : 0;
   // TMEM key stash: warp w owns lanes 32*(w%4).., columns (w/4)*ITEMS..
-  constexpr bool STASH = OS_TMEM_STASH && KB == 4 && (!HAS_V || VB == 4) && ITEMS % 8 == 0 &&
-                         WARPS % 4 == 0;
-  constexpr int NW = HAS_V ? 2 : 1;  // stashed words per item: key (+ value)
+  constexpr bool STASH = OS_TMEM_STASH && (KB == 4 || (KB == 8 && OS_STASH64)) &&
+                         (!HAS_V || VB == 4) && ITEMS % 8 == 0 && WARPS % 4 == 0;
+  constexpr int KW = KB / 4;                 // TMEM words per key
+  constexpr int NW = KW + (HAS_V ? 1 : 0);   // stashed words per item: key (+ value)
   constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * ITEMS * NW;
   constexpr uint32_t TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                            : TCOLS_RAW <= 256 ? 256 : 512;
@@ -289,6 +293,26 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   K keys[STASH ? 1 : ITEMS];        // encoded keys, kept for the reorder
   uint32_t kc[8];                   // TMEM stash chunk (keys)
   uint32_t vc[8];                   // TMEM stash chunk (values)
+  // keys go to columns [0, ITEMS*KW) of the warp's range, 8 words per store
+  auto stash_key = [&](int i, K x) {
+    if constexpr (KW == 1) {
+      kc[i & 7] = uint32_t(x);
+      if ((i & 7) == 7) tmem_st8(taddr + uint32_t(i - 7), kc);
+    } else {
+      kc[2 * (i & 3)] = uint32_t(uint64_t(x));
+      kc[2 * (i & 3) + 1] = uint32_t(uint64_t(x) >> 32);
+      if ((i & 3) == 3) tmem_st8(taddr + uint32_t(2 * (i - 3)), kc);
+    }
+  };
+  auto unstash_key = [&](int i) -> K {
+    if constexpr (KW == 1) {
+      if ((i & 7) == 0) tmem_ld8(taddr + uint32_t(i), kc);
+      return K(kc[i & 7]);
+    } else {
+      if ((i & 3) == 0) tmem_ld8(taddr + uint32_t(2 * i), kc);
+      return K(uint64_t(kc[2 * (i & 3)]) | (uint64_t(kc[2 * (i & 3) + 1]) << 32));
+    }
+  };
   uint32_t ranks[(ITEMS + 1) / 2];  // two u16 scaled ranks per register
   const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
   auto rank_items = [&](auto full_tag) {
@@ -300,10 +324,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       const uint32_t idx = warp_base + i * 32 + lane;
       const K x = CODED ? cin(s_keys[idx]) : s_keys[idx];
       if constexpr (OS_KEYS_IN_REGS && !STASH) keys[i] = x;
-      if (STASH) {
-        kc[i & 7] = uint32_t(x);
-        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(i - 7), kc);
-      }
+      if constexpr (STASH) stash_key(i, x);
       uint32_t d;
       if (FULL)
         d = digit(x);
@@ -353,8 +374,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
           for (int i = 0; i < ITEMS; ++i) {
             const K x = s_keys[warp_base + i * 32 + lane];
-            kc[i & 7] = uint32_t(CODED ? cin(x) : x);
-            if ((i & 7) == 7) tmem_st8(taddr + uint32_t(i - 7), kc);
+            stash_key(i, CODED ? cin(x) : x);
           }
         }
       }
@@ -425,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         kc[i & 7] = uint32_t(s_vals[warp_base + i * 32 + lane]);
-        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(ITEMS + i - 7), kc);
+        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(ITEMS * KW + i - 7), kc);
       }
       tmem_wait_st();
     } else {
@@ -453,9 +473,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        if (STASH && (i & 7) == 0) tmem_ld8(taddr + uint32_t(i), kc);
-        if (STASH && HAS_V && (i & 7) == 0) tmem_ld8(taddr + uint32_t(ITEMS + i), vc);
-        const K key = STASH ? K(kc[i & 7]) : keys[STASH ? 0 : i];
+        if (STASH && HAS_V && (i & 7) == 0) tmem_ld8(taddr + uint32_t(ITEMS * KW + i), vc);
+        K key;
+        if constexpr (STASH)
+          key = unstash_key(i);
+        else
+          key = keys[i];
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
         const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
         const uint32_t off = lds_u16(fma_u32(digit(key), k_two, hbase));
@@ -640,14 +663,16 @@ template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I =
 template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
 template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
 #ifndef OS_P32_T
-#define OS_P32_T 256  // tools/bench_configs.py: 1212 us/pass at q=1 vs 1245 with 512 x 16
+#define OS_P32_T 256  // keys + values in TMEM, 3 blocks/SM: 1128 us/pass at q=1 (was 1222 at 2/SM)
 #define OS_P32_I 32
 #define OS_P32_B 3
 #endif
 #ifndef OS_K64_T
-#define OS_K64_T 256  // tools/bench_configs.py: 1687 us/pass vs 2045 with 512 x 8
-#define OS_K64_I 16
-#define OS_K64_B 3
+// keys + values in TMEM: 256 x 32 at 2 blocks/SM, 1520 us/pass (C4, 20.7 GKey/s)
+// vs 256 x 16 at 3 blocks/SM without the stash, 1640 us/pass
+#define OS_K64_T 256
+#define OS_K64_I 32
+#define OS_K64_B 2
 #endif
 template <> struct Geometry<4, 4> { static constexpr int T = OS_P32_T, I = OS_P32_I, B = OS_P32_B; };
 template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; };

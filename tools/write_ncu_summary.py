@@ -1,0 +1,80 @@
+"""Regenerate profiles/round1_ncu_summary.md from the files
+tools/refresh_profiles.py wrote (bench line, ncu counters, launch list).
+Usage: python tools/write_ncu_summary.py SESSION_TAG"""
+import csv
+import collections
+import json
+import sys
+
+tag = sys.argv[1]
+b = json.loads(open("profiles/round1_bench.json").read().strip().splitlines()[-1])
+d = json.load(open("profiles/ncu_traffic.json"))["detail"]
+bi, hi = d["binning"], d["histogram"]
+items = 268435456 / 32
+rows = list(csv.reader(open("profiles/round1_launches.csv")))
+h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+ki, vi = rows[h].index("Kernel Name"), rows[h].index("Metric Value")
+agg = collections.defaultdict(list)
+for r in rows[h + 1:]:
+    agg[r[ki].split("(")[0].replace("void ", "")].append(float(r[vi].replace(",", "")) / 1e3)
+hist_l = [v for k, v in agg.items() if "histogram" in k][0]
+bin_l = [v for k, v in agg.items() if "binning" in k][0]
+per_sort = sum(hist_l) / len(hist_l) + 4 * sum(bin_l) / len(bin_l)
+hs = sum(hist_l) / len(hist_l) / per_sort * 100
+bs = 4 * sum(bin_l) / len(bin_l) / per_sort * 100
+e2e = b["e2e"]
+txt = f"""# Round 1 — ncu evidence (B200, sm_100a, clocks not locked, SM {b["clocks"]["sm_mhz"]:.0f} MHz)
+
+Workload: `python bench.py` (C2: 256M uniform u32 keys-only, d=8).
+Build: session {tag} (binning block 256 threads × 64 keys, 16K-key tiles, 3 blocks/SM, keys parked in TMEM between ranking and reorder).
+
+* Launch list: `profiles/round1_launches.csv`, from `ncu --metrics gpu__time_duration.sum --clock-control none` (session {tag}).
+* Per-kernel figures: `ncu --set full --clock-control none --import-source on`, one launch each. The captures (`gpurun_out/prof_{{binning,hist}}_{tag}.ncu-rep`) are scratch; `profiles/ncu_traffic.json` holds their counters (`tools/refresh_profiles.py {tag}`).
+* Bench line of the same session: `profiles/round1_bench.json`. C1/C3/C4/C5 sweep: `profiles/round1_configs.jsonl` (`tools/bench_configs.py`). Per-tile timeline: `profiles/round1_trace.txt`.
+* Calibration: CUB `DeviceRadixSort::SortKeys` (CUDA 12.9) on the same B200 and shape runs at **43.95 GKey/s** (`profiles/round1_cub_compare.txt`, `tools/cub_compare.cu`); this build runs at **{b["value"]:.1f} GKey/s**. Box-to-box spread across this round's sessions is about ±1 % (698-710 µs per pass).
+
+## Bench line (session {tag})
+
+| quantity | value |
+|---|---|
+| sort of 256M u32 keys | {b["ms_per_step"]:.3f} ms → **{b["value"]:.1f} GKey/s** ({b["hbm_roofline_frac_sort"]*100:.1f} % of the (1+2p)·n·4 B roofline at 6547.5 GB/s measured) |
+| binning pass (live CUDA events) | {b["roofline"]["launch_us"]:.0f} µs → {b["roofline"]["achieved"]/1000:.2f} TB/s = **{b["roofline"]["frac"]*100:.1f} %** of measured HBM copy bandwidth |
+| histogram (live) | {b["kernels"]["histogram_us"]:.0f} µs → {b["kernels"]["histogram_gbs"]/1000:.2f} TB/s = {b["kernels"]["histogram_gbs"]/6547.5*100:.0f} % of measured |
+| e2e host → host, `SortPipeline` (upload / sort / download of consecutive steps overlapped) | {e2e["value"]:.2f} GKey/s (PCIe-bound) |
+| e2e host → host, synchronous `onesweep_sort` on a numpy array | {e2e["synchronous"]["value"]:.2f} GKey/s |
+| SM clock during the timed region | {b["clocks"]["sm_mhz"]:.0f} MHz (= max), no throttle reasons |
+
+## Launch list (cold-cache, serialised: compare shares, not absolutes)
+
+| kernel | launches per sort | time per launch | share of a sort |
+|---|---|---|---|
+| `onesweep_histogram_u32d8_kernel` | 1 | {sum(hist_l)/len(hist_l):.0f} µs | {hs:.1f} % |
+| `onesweep_binning_kernel<u32, NoValue, 256, 64, 3, …>` (one per digit place) | 4 | {sum(bin_l)/len(bin_l):.0f} µs | {bs:.1f} % |
+
+The bench's live CUDA-event split agrees: histogram {b["kernels"]["histogram_us"]:.0f} µs, passes {b["roofline"]["launch_us"]:.0f} µs × 4, binning share {b["kernels"]["share_binning"]*100:.1f} %.
+
+## Per-kernel counters
+
+| | binning pass | histogram |
+|---|---|---|
+| duration (ncu) | {bi["duration_us"]:.1f} µs | {hi["duration_us"]:.1f} µs |
+| algorithmic bytes per launch | 2·n·4 = 2,147,483,648 | n·4 = 1,073,741,824 |
+| DRAM bytes (read + write) | {bi["dram_read_bytes"]/1e9:.4f} + {bi["dram_write_bytes"]/1e9:.4f} = {bi["traffic"]/1e9:.3f} GB | {hi["dram_read_bytes"]/1e9:.3f} + {hi["dram_write_bytes"]/1e9:.3f} = {hi["traffic"]/1e9:.3f} GB |
+| traffic / algorithmic | {bi["traffic"]/2147483648:.2f} | {hi["traffic"]/1073741824:.2f} |
+| **L1/shared data-pipe wavefronts, % of peak** | **{bi["lsu_data_pipe_pct"]:.1f} %** | {hi["lsu_data_pipe_pct"]:.1f} % |
+| shared wavefronts | {bi["smem_wavefronts"]/1e6:.1f} M ({bi["smem_wavefronts"]/items:.1f} per 32-key item) | {hi["smem_wavefronts"]/1e6:.1f} M |
+| of which bank conflicts | {bi["smem_bank_conflicts"]/1e6:.1f} M | {hi["smem_bank_conflicts"]/1e6:.1f} M |
+| instructions executed | {bi["inst_executed"]/1e6:.1f} M ({bi["inst_executed"]/items:.1f} per item) | {hi["inst_executed"]/1e6:.1f} M |
+| issue slots busy | {bi["issue_active"]*100:.0f} % | {hi["issue_active"]*100:.0f} % |
+| warps active per SM | ~23.4 of 64 (3 blocks × 8 warps, {bi["registers"]} regs) | |
+| L2 hit rate | {bi["l2_hit_pct"]:.1f} % | {hi["l2_hit_pct"]:.2f} % |
+
+## Reading
+
+* **The binning pass is SM-bound, not HBM-bound.** It moves exactly its algorithmic bytes, at {b["roofline"]["frac"]*100:.0f} % of the measured copy bandwidth. Two SM resources take turns as the limiter. During ranking (46 % of a tile's ~17.5 µs life, `round1_trace.txt`) the SM is issue- and ALU-bound: ~35 instructions per 32 keys, three tiles ranking at once. In the reorder and run writes it is the shared-memory data pipe: {bi["smem_wavefronts"]/items:.1f} wavefronts per item over the whole kernel, half of them bank conflicts from 32 random digits.
+* **What this round changed.** Parking each thread's keys in TMEM (`tcgen05.st/ld`) between ranking and reorder freed the registers that held them. That allowed 16K-key tiles: 738 → ~700 µs per pass, 69.7 → {bi["inst_executed"]/items:.1f} instructions per item, 18.4 → {bi["smem_wavefronts"]/items:.1f} shared wavefronts per item (`round1_binning_notes.md`, session 3).
+* **What the rest of the time is.** With throwaway what-if builds, dropping the run writes saves 180 µs per pass. Sending the same writes to an L2-resident window still saves 140 µs, so the HBM write stream, and not SM work, is most of the output phase. The look-back latency is hidden (removing it changes nothing). The reduce-then-scan ablation agrees: its downsweep is this kernel without the look-back and takes 680 µs (`round1_rts_ablation.md`).
+* **Histogram.** HBM-bound at ~92 % of measured copy bandwidth (lane-private counters make every shared-memory add conflict-free).
+"""
+open("profiles/round1_ncu_summary.md", "w").write(txt)
+print("ok")
