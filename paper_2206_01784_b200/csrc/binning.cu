@@ -56,18 +56,6 @@ template <> struct ValTraits<NoValue> {
 #define OS_LOOKBACK_WINDOW 4
 #endif
 constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
-// 1: keys stay in registers from the ranking loop to the reorder (one shared
-// load per key less, more registers); 0: re-read before the reorder.
-#ifndef OS_KEYS_IN_REGS
-#define OS_KEYS_IN_REGS 0
-#endif
-
-// 1: the first look-back window is loaded before the reorder and consumed
-// after it, so its round trip overlaps the reorder.
-#ifndef OS_EARLY_LOOKBACK
-#define OS_EARLY_LOOKBACK 0
-#endif
-
 // Per-tile timeline records (os_debug_trace) are compiled in only for
 // diagnostic builds (-DOS_TRACE=1); the product kernel carries no trace code.
 #ifndef OS_TRACE
@@ -93,9 +81,6 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #endif
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
-#endif
-#ifndef OS_FMA_ADDS
-#define OS_FMA_ADDS 0
 #endif
 
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
@@ -169,11 +154,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const uint32_t byte_sel = 0x4440u | uint32_t((shift & 31) >> 3);
   const bool hi_word = shift >= 32;
   const uint32_t smem_base = smem_u32(smem_raw);
-  // opaque small constants for FMA-pipe integer arithmetic (see fma_u32);
-  // OS_FMA_ADDS=0 leaves the adds to the compiler (ALU-pipe IADD3/LEA)
-  const uint32_t k_one = OS_FMA_ADDS ? opaque_all_ones() >> 31 : 1u;
-  const uint32_t k_two = k_one + k_one;
-  const uint32_t k_shl16 = k_one << 16;
+  // multiply-add operands for the index arithmetic (see fma_u32): written as
+  // mad.lo, ptxas keeps these as IMADs on the FMA pipe (742 vs 808 us/pass,
+  // profiles/round1_binning_notes.md)
+  constexpr uint32_t k_one = 1u, k_two = 2u, k_shl16 = 1u << 16;
 
   if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
   if (tid == 0) {
@@ -323,7 +307,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       const K x = CODED ? cin(s_keys[idx]) : s_keys[idx];
-      if constexpr (OS_KEYS_IN_REGS && !STASH) keys[i] = x;
       if constexpr (STASH) stash_key(i, x);
       uint32_t d;
       if (FULL)
@@ -431,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   }
   // keys and values into registers; after the barrier the tile buffers are
   // rewritten in place as per-digit runs
-  if constexpr (!OS_KEYS_IN_REGS && !STASH) {
+  if constexpr (!STASH) {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const K x = s_keys[warp_base + i * 32 + lane];
@@ -452,15 +435,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) vals[i] = s_vals[warp_base + i * 32 + lane];
     }
-  }
-  // first look-back window, in flight during the reorder (OS_EARLY_LOOKBACK)
-  uint32_t lbw[kLookbackWindow];
-  if (OS_EARLY_LOOKBACK && tid < radix && tile > 0) {
-#pragma unroll
-    for (int k = 0; k < kLookbackWindow; ++k)
-      lbw[k] = (int(tile) - 1 - k >= 0)
-                   ? ld_relaxed_gpu(P.status + size_t(int(tile) - 1 - k) * radix + tid)
-                   : kFlagGlobal;
   }
   __syncthreads();
   const int fast = s_fast;
@@ -514,13 +488,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       const uint32_t* p = P.status + size_t(tile - 1) * stride + tid;
       int j = int(tile) - 1;
       bool done = false;
-      bool first = true;
       while (!done) {
         uint32_t w[kLookbackWindow];
-        if (OS_EARLY_LOOKBACK && first) {
-#pragma unroll
-          for (int k = 0; k < kLookbackWindow; ++k) w[k] = lbw[k];
-        } else if (j >= kLookbackWindow - 1) {
+        if (j >= kLookbackWindow - 1) {
 #pragma unroll
           for (int k = 0; k < kLookbackWindow; ++k) w[k] = ld_relaxed_gpu(p - k * stride);
         } else {
@@ -528,7 +498,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           for (int k = 0; k < kLookbackWindow; ++k)
             w[k] = (j - k >= 0) ? ld_relaxed_gpu(p - k * stride) : kFlagGlobal;
         }
-        first = false;
         reads += kLookbackWindow;
         ++rounds;
         int k = 0;
