@@ -53,7 +53,7 @@ template <> struct ValTraits<NoValue> {
 
 // Predecessor status words read per look-back round trip (lookback.py:144-169).
 #ifndef OS_LOOKBACK_WINDOW
-#define OS_LOOKBACK_WINDOW 4
+#define OS_LOOKBACK_WINDOW 6  // 16K tiles: 707 us (6, 8) vs 711 (4), 716 (3), 727 (2)
 #endif
 constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 // Per-tile timeline records (os_debug_trace) are compiled in only for
