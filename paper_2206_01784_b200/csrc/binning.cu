@@ -65,9 +65,11 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 // counter write, and that write before the next item's read.  The accesses
 // are volatile, so they keep program order, and the warp is converged (no
 // divergent branches in the loop), so they also execute in order.
-// OS_SYNCWARP=1 adds the formal __syncwarp() fences (two NOPs per item).
+// OS_SYNCWARP adds the formal __syncwarp() fences (bit 0: read -> leader write,
+// bit 1: leader write -> next read; one NOP each).  Timing: both 706 us,
+// bit 0 only 705, bit 1 only 710, none 707 (noise level); both are kept.
 #ifndef OS_SYNCWARP
-#define OS_SYNCWARP 1
+#define OS_SYNCWARP 3
 #endif
 
 // Skip the multisplit for warps whose 32*ITEMS keys share one digit.
@@ -322,9 +324,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         ranks[i / 2] = fma_u32(rank, k_shl16, ranks[i / 2]);
       else
         ranks[i / 2] = rank;
-      if (OS_SYNCWARP) __syncwarp();
+      if (OS_SYNCWARP & 1) __syncwarp();
       if (leader) sts_u16(caddr, rank);
-      if (OS_SYNCWARP) __syncwarp();
+      if (OS_SYNCWARP & 2) __syncwarp();
     }
   };
   // A warp whose keys all carry one digit needs no multisplit: its inclusive
