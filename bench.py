@@ -269,8 +269,8 @@ def run_ours(args) -> None:
         "config": {
             "workload": ("C2: 256M uniform u32 keys-only, 8-bit digits, 1 histogram + 4 binning passes"
                          if world == 1 else
-                         f"C5-style sharded sort: {n} u32 keys per GPU, MSD split + NCCL all-to-all "
-                         "+ local Onesweep"),
+                         f"C5-style sharded sort: {n} u32 keys per GPU, MSD split + "
+                         f"{getattr(sorter, 'exchange', 'all_to_all')} exchange + local Onesweep"),
             "n_per_gpu": n,
             "digit_bits": 8,
             "tile_keys": getattr(sorter, "tile", None),

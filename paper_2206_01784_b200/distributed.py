@@ -189,6 +189,10 @@ class SymmetricReceive:
 
         self.cap, self.elem_bytes = cap, elem_bytes
         name = (group or dist.group.WORLD).group_name
+        try:  # required by some torch versions, a no-op (or absent) in others
+            symm_mem.enable_symm_mem_for_group(name)
+        except Exception:  # noqa: BLE001
+            pass
         self.buf = symm_mem.empty(2 * cap * elem_bytes, dtype=torch.uint8, device=device)
         self.handle = symm_mem.rendezvous(self.buf, name)
         self.peer_ptrs = [int(p) for p in self.handle.buffer_ptrs]
@@ -336,9 +340,14 @@ def emulate_p2p_sort(shards, value_shards=None, *, ops=None, digit_bits: int = S
 
 
 class ShardedSorter:
-    """Bench helper: a sharded sort of `n` keys per rank."""
+    """Bench helper: a sharded sort of `n` keys per rank.
 
-    def __init__(self, n: int, key_dtype, device=None, group=None):
+    On construction it sorts a small probe with the fused p2p exchange and
+    with the all-to-all, and keeps p2p only if every rank got identical
+    results from both (so an unusable peer mapping degrades to all-to-all
+    instead of failing the run)."""
+
+    def __init__(self, n: int, key_dtype, device=None, group=None, probe: int = 1 << 16):
         from .keycodec import radix_plan
 
         self.n = n
@@ -347,6 +356,32 @@ class ShardedSorter:
         self.local_passes = radix_plan(self.spec.bits, 8).passes
         strips = -(-2 * n // (1 << 28))  # receive side may exceed n under skew
         self.launches_per_step = 1 + 1 + 1 + self.local_passes * strips  # msd hist, map, partition, local
+        self.exchange = self._choose_exchange(key_dtype, device, probe)
+
+    def _choose_exchange(self, key_dtype, device, probe: int) -> str:
+        import torch
+        import torch.distributed as dist
+
+        dev = torch.device(device or "cuda")
+        if dist.get_backend(self.group) != "nccl":
+            return "all_to_all"
+        g = torch.Generator(device="cpu").manual_seed(1234 + dist.get_rank(self.group))
+        k = torch.randint(0, 2**31 - 1, (probe,), generator=g, dtype=torch.int64)
+        k = k.to(torch.int32).view(torch.uint32).to(dev) if key_dtype == torch.uint32 else \
+            k.to(dev).to(key_dtype)
+        ok = 1
+        try:
+            a = sharded_sort(k, None, self.group, exchange="p2p")
+            b = sharded_sort(k, None, self.group, exchange="all_to_all")
+            ok = int(a.numel() == b.numel() and bool(torch.equal(a, b)))
+        except Exception as e:  # noqa: BLE001 -- any failure selects the fallback
+            import warnings
+
+            warnings.warn(f"p2p exchange probe failed ({e}); using all_to_all")
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return "p2p" if int(flag.item()) == 1 else "all_to_all"
 
     def __call__(self, keys, values=None):
-        return sharded_sort(keys, values, self.group)
+        return sharded_sort(keys, values, self.group, exchange=self.exchange)
