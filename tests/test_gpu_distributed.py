@@ -170,3 +170,20 @@ def test_p2p_rejects_mixed_widths(cuda):
     v = torch.zeros(1000, dtype=torch.int64, device="cuda")
     with pytest.raises(ValueError):
         emulate_p2p_sort([k, k], [v, v])
+
+
+def test_p2p_symmetric_memory_plumbing_world1(cuda):
+    """The fused exchange's real host plumbing on one GPU: a world-size-1 NCCL
+    group, torch symmetric memory (empty / rendezvous / buffer_ptrs /
+    barrier) and sharded_sort(exchange="p2p") against onesweep_sort, and the
+    ShardedSorter probe selecting p2p (tools/p2p_probe.py, in a subprocess so
+    the process group stays private)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "p2p_probe.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "exchange p2p keys equal True values equal True" in r.stdout
+    assert "ShardedSorter exchange: p2p" in r.stdout
