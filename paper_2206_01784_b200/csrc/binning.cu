@@ -81,6 +81,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #ifndef OS_TMEM_STASH
 #define OS_TMEM_STASH 1
 #endif
+#ifndef OS_STATUS_KEEP
+#define OS_STATUS_KEEP 0  // 1: status words carry an L2 evict_last policy (tools/gpu_status_l2.sh; 709 vs 707 us)
+#endif
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
 #endif
@@ -160,6 +163,17 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // mad.lo, ptxas keeps these as IMADs on the FMA pipe (742 vs 808 us/pass,
   // profiles/round1_binning_notes.md)
   constexpr uint32_t k_one = 1u, k_two = 2u, k_shl16 = 1u << 16;
+  // look-back status words (lookback.py:63-79), optionally kept in L2
+  const uint64_t status_pol = OS_STATUS_KEEP ? l2_policy_evict_last() : 0ull;
+  auto status_ld = [&](const uint32_t* a) -> uint32_t {
+    return OS_STATUS_KEEP ? ld_relaxed_gpu_keep(a, status_pol) : ld_relaxed_gpu(a);
+  };
+  auto status_st = [&](uint32_t* a, uint32_t v) {
+    if (OS_STATUS_KEEP)
+      st_relaxed_gpu_keep(a, v, status_pol);
+    else
+      st_relaxed_gpu(a, v);
+  };
 
   if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
   if (tid == 0) {
@@ -383,8 +397,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
     if (P.rts_offsets == nullptr)  // (reduce-then-scan passes have no look-back)
-      st_relaxed_gpu(P.status + size_t(tile) * radix + tid,
-                     (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+      status_st(P.status + size_t(tile) * radix + tid,
+                (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
   }
   if (OS_TRACE && trace && tid == 0) trace[2] = global_ns();
@@ -494,11 +508,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         uint32_t w[kLookbackWindow];
         if (j >= kLookbackWindow - 1) {
 #pragma unroll
-          for (int k = 0; k < kLookbackWindow; ++k) w[k] = ld_relaxed_gpu(p - k * stride);
+          for (int k = 0; k < kLookbackWindow; ++k) w[k] = status_ld(p - k * stride);
         } else {
 #pragma unroll
           for (int k = 0; k < kLookbackWindow; ++k)
-            w[k] = (j - k >= 0) ? ld_relaxed_gpu(p - k * stride) : kFlagGlobal;
+            w[k] = (j - k >= 0) ? status_ld(p - k * stride) : kFlagGlobal;
         }
         reads += kLookbackWindow;
         ++rounds;
@@ -519,7 +533,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         j -= k;
         p -= k * stride;
       }
-      st_relaxed_gpu(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
+      status_st(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
     if (OS_TRACE && trace && tid == 0) trace[4] = global_ns();
     // reduce-then-scan ablation (rts.cu): the tile's run starts come from the

@@ -215,6 +215,17 @@ __device__ __forceinline__ void named_barrier_sync(int id, int threads) {
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// Status-word accesses with an L2 evict_last policy: nothing else in the
+// kernels uses that policy, so ncu's lts__t_sectors_*_evict_last_* counters
+// isolate the look-back traffic (its L2 hit rate), and the words stay resident.
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_keep(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_keep(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -251,6 +262,11 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
 template <typename T>
 __device__ __forceinline__ T* elem_at(T* base, unsigned long long index) {
   return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(base) + index * sizeof(T));
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
