@@ -39,6 +39,7 @@ Build: session {tag} (binning block 256 threads × 64 keys, 16K-key tiles, 3 blo
 |---|---|
 | sort of 256M u32 keys | {b["ms_per_step"]:.3f} ms → **{b["value"]:.1f} GKey/s** ({b["hbm_roofline_frac_sort"]*100:.1f} % of the (1+2p)·n·4 B roofline at 6547.5 GB/s measured) |
 | binning pass (live CUDA events) | {b["roofline"]["launch_us"]:.0f} µs → {b["roofline"]["achieved"]/1000:.2f} TB/s = **{b["roofline"]["frac"]*100:.1f} %** of measured HBM copy bandwidth |
+| the same against the ~8 TB/s nominal HBM3e figure (north_star) | sort {b["hbm_roofline_frac_sort"]*6547.5/8000*100:.1f} %, binning pass {b["roofline"]["achieved"]/8000*100:.1f} % |
 | histogram (live) | {b["kernels"]["histogram_us"]:.0f} µs → {b["kernels"]["histogram_gbs"]/1000:.2f} TB/s = {b["kernels"]["histogram_gbs"]/6547.5*100:.0f} % of measured |
 | e2e host → host, `SortPipeline` (upload / sort / download of consecutive steps overlapped) | {e2e["value"]:.2f} GKey/s (PCIe-bound) |
 | e2e host → host, synchronous `onesweep_sort` on a numpy array | {e2e["synchronous"]["value"]:.2f} GKey/s |
