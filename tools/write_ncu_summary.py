@@ -26,12 +26,12 @@ e2e = b["e2e"]
 txt = f"""# Round 1 — ncu evidence (B200, sm_100a, clocks not locked, SM {b["clocks"]["sm_mhz"]:.0f} MHz)
 
 Workload: `python bench.py` (C2: 256M uniform u32 keys-only, d=8).
-Build: session {tag} (binning block 256 threads × 64 keys, 16K-key tiles, 3 blocks/SM, keys parked in TMEM between ranking and reorder).
+Build: session {tag} (binning block 256 threads × 40 keys, 10K-key tiles, 4 blocks/SM, keys parked in TMEM between ranking and reorder).
 
 * Launch list: `profiles/round1_launches.csv`, from `ncu --metrics gpu__time_duration.sum --clock-control none` (session {tag}).
 * Per-kernel figures: `ncu --set full --clock-control none --import-source on`, one launch each. The captures (`gpurun_out/prof_{{binning,hist}}_{tag}.ncu-rep`) are scratch; `profiles/ncu_traffic.json` holds their counters (`tools/refresh_profiles.py {tag}`).
 * Bench line of the same session: `profiles/round1_bench.json`. C1/C3/C4/C5 sweep: `profiles/round1_configs.jsonl` (`tools/bench_configs.py`). Per-tile timeline: `profiles/round1_trace.txt`.
-* Calibration: CUB `DeviceRadixSort::SortKeys` (CUDA 12.9) on the same B200 and shape runs at **43.95 GKey/s** (`profiles/round1_cub_compare.txt`, `tools/cub_compare.cu`); this build runs at **{b["value"]:.1f} GKey/s**. Box-to-box spread across this round's sessions is about ±1 % (698-710 µs per pass).
+* Calibration: CUB `DeviceRadixSort::SortKeys` (CUDA 12.9) on the same B200 and shape runs at **43.95 GKey/s** (`profiles/round1_cub_compare.txt`, `tools/cub_compare.cu`); this build runs at **{b["value"]:.1f} GKey/s**. Box-to-box spread across this round's sessions is about ±1 %.
 
 ## Bench line (session {tag})
 
@@ -50,7 +50,7 @@ Build: session {tag} (binning block 256 threads × 64 keys, 16K-key tiles, 3 blo
 | kernel | launches per sort | time per launch | share of a sort |
 |---|---|---|---|
 | `onesweep_histogram_u32d8_kernel` | 1 | {sum(hist_l)/len(hist_l):.0f} µs | {hs:.1f} % |
-| `onesweep_binning_kernel<u32, NoValue, 256, 64, 3, …>` (one per digit place) | 4 | {sum(bin_l)/len(bin_l):.0f} µs | {bs:.1f} % |
+| `onesweep_binning_kernel<u32, NoValue, 256, 40, 4, …>` (one per digit place) | 4 | {sum(bin_l)/len(bin_l):.0f} µs | {bs:.1f} % |
 
 The bench's live CUDA-event split agrees: histogram {b["kernels"]["histogram_us"]:.0f} µs, passes {b["roofline"]["launch_us"]:.0f} µs × 4, binning share {b["kernels"]["share_binning"]*100:.1f} %.
 
@@ -67,15 +67,15 @@ The bench's live CUDA-event split agrees: histogram {b["kernels"]["histogram_us"
 | of which bank conflicts | {bi["smem_bank_conflicts"]/1e6:.1f} M | {hi["smem_bank_conflicts"]/1e6:.1f} M |
 | instructions executed | {bi["inst_executed"]/1e6:.1f} M ({bi["inst_executed"]/items:.1f} per item) | {hi["inst_executed"]/1e6:.1f} M |
 | issue slots busy | {bi["issue_active"]*100:.0f} % | {hi["issue_active"]*100:.0f} % |
-| warps active per SM | ~23.4 of 64 (3 blocks × 8 warps, {bi["registers"]} regs) | |
+| warps active per SM | ≤ 32 of 64 (4 blocks × 8 warps, {bi["registers"]} regs) | |
 | L2 hit rate | {bi["l2_hit_pct"]:.1f} % | {hi["l2_hit_pct"]:.2f} % |
 
 ## Reading
 
-* **The binning pass is SM-bound, not HBM-bound.** It moves exactly its algorithmic bytes, at {b["roofline"]["frac"]*100:.0f} % of the measured copy bandwidth. Two SM resources take turns as the limiter. During ranking (46 % of a tile's ~17.5 µs life, `round1_trace.txt`) the SM is issue- and ALU-bound: ~35 instructions per 32 keys, three tiles ranking at once. In the reorder and run writes it is the shared-memory data pipe: {bi["smem_wavefronts"]/items:.1f} wavefronts per item over the whole kernel, half of them bank conflicts from 32 random digits.
-* **What this round changed.** Parking each thread's keys in TMEM (`tcgen05.st/ld`) between ranking and reorder freed the registers that held them. That allowed 16K-key tiles: 738 → ~700 µs per pass, 69.7 → {bi["inst_executed"]/items:.1f} instructions per item, 18.4 → {bi["smem_wavefronts"]/items:.1f} shared wavefronts per item (`round1_binning_notes.md`, session 3).
-* **What the rest of the time is.** With throwaway what-if builds, dropping the run writes saves 180 µs per pass. Sending the same writes to an L2-resident window still saves 140 µs, so the HBM write stream, and not SM work, is most of the output phase. The look-back latency is hidden (removing it changes nothing). The reduce-then-scan ablation agrees: its downsweep is this kernel without the look-back and takes 680 µs (`round1_rts_ablation.md`).
-* **L2 hit rate of the look-back status words: ~90 %.** Measured by tagging every status load and store with an L2 evict_last policy. Nothing else in the kernels uses that policy, so the evict_last sector counters isolate the look-back traffic: `lts__t_sectors_srcunit_tex_evict_last_lookup_hit/miss` = 8.80 M / 0.93 M sectors per pass, 90.5 %, i.e. ~311 MB of status traffic per pass, nearly all served by L2 (`tools/gpu_status_l2.sh`, `profiles/round1_status_l2.csv`, 4 launches). The misses are first touches of each tile's row. The policy itself is timing-neutral (709 vs 707 µs), so the product build leaves it off (`OS_STATUS_KEEP`).
+* **The binning pass is SM-bound, not HBM-bound.** It moves exactly its algorithmic bytes, at {b["roofline"]["frac"]*100:.0f} % of the measured copy bandwidth. Two SM resources take turns as the limiter. During ranking (46 % of a tile's ~13 µs life, `round1_trace.txt`) the SM is issue- and ALU-bound: ~35 instructions per 32 keys, four tiles ranking at once. In the reorder and run writes it is the shared-memory data pipe: {bi["smem_wavefronts"]/items:.1f} wavefronts per item over the whole kernel, half of them bank conflicts from 32 random digits.
+* **What this round changed.** Parking each thread's keys in TMEM (`tcgen05.st/ld`) between ranking and reorder freed the registers that held them. That allowed larger tiles and then a fourth tile per SM: 738 → 693 µs per pass, 69.7 → {bi["inst_executed"]/items:.1f} instructions per item, 18.4 → {bi["smem_wavefronts"]/items:.1f} shared wavefronts per item (`round1_binning_notes.md`, session 3).
+* **What the rest of the time is.** With throwaway what-if builds, dropping the run writes saves 180 µs per pass. Sending the same writes to an L2-resident window still saves 140 µs, so the HBM write stream, and not SM work, is most of the output phase. The look-back latency is hidden (removing it changes nothing). The reduce-then-scan ablation agrees: its downsweep is this kernel without the look-back and takes 653 µs against 693 (`round1_rts_ablation.md`).
+* **L2 hit rate of the look-back status words: ~90 %.** Measured by tagging every status load and store with an L2 evict_last policy. Nothing else in the kernels uses that policy, so the evict_last sector counters isolate the look-back traffic: `lts__t_sectors_srcunit_tex_evict_last_lookup_hit/miss` = 16.7 M / 1.47 M sectors per pass at 10K-key tiles, 91.9 %, i.e. ~580 MB of status traffic per pass, nearly all served by L2 (`tools/gpu_status_l2.sh`, `profiles/round1_status_l2.csv`, 4 launches). The misses are first touches of each tile's row. The policy itself is timing-neutral (709 vs 707 µs at 16K tiles), so the product build leaves it off (`OS_STATUS_KEEP`).
 * **Histogram.** HBM-bound at ~92 % of measured copy bandwidth (lane-private counters make every shared-memory add conflict-free).
 """
 open("profiles/round1_ncu_summary.md", "w").write(txt)
