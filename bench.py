@@ -335,20 +335,21 @@ def run_ours(args) -> None:
             # moves its 1 GiB in and its 1 GiB out over PCIe)
             from paper_2206_01784_b200 import SortPipeline
 
-            pipe = SortPipeline(n, torch.uint32)
-            outs_h = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
-            for j in range(2):  # warm-up
-                pipe.submit(keys_h, outs_h[j % 2])
+            depth = 3  # tools/pipe_probe.py: 24.3 / 23.3 / 23.3 ms per step at depth 2 / 3 / 4
+            pipe = SortPipeline(n, torch.uint32, depth=depth)
+            outs_h = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(depth)]
+            for j in range(depth):  # warm-up
+                pipe.submit(keys_h, outs_h[j % depth])
             pipe.synchronize()
-            steps_p = max(2 * args.e2e_steps, 8)
+            steps_p = max(4 * args.e2e_steps, 16)  # pipeline fill and drain are inside the timing
             t0 = time.perf_counter()
             for j in range(steps_p):
-                pipe.submit(keys_h, outs_h[j % 2])
+                pipe.submit(keys_h, outs_h[j % depth])
             pipe.synchronize()
             t1 = time.perf_counter()
             e2e_p = (t1 - t0) / steps_p
-            ok = bool((outs_h[(steps_p - 1) % 2][: 1 << 20].numpy()[1:] >=
-                       outs_h[(steps_p - 1) % 2][: 1 << 20].numpy()[:-1]).all())
+            last = outs_h[(steps_p - 1) % depth][: 1 << 20].numpy()
+            ok = bool((last[1:] >= last[:-1]).all())
             line["e2e"] = {"value": n / e2e_p / 1e9, "unit": "GKey/s", "h2d_bytes_per_step": n * kb,
                            "d2h_bytes_per_step": n * kb, "ms_per_step": e2e_p * 1e3, "steps": steps_p,
                            "output_sorted_prefix": ok,
