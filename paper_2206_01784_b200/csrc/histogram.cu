@@ -22,7 +22,10 @@ namespace osb {
 
 constexpr int kHistThreads = 1024;
 constexpr int kHistWarps = kHistThreads / 32;
-constexpr int kHistVec = 4;                       // 16-byte vectors per thread per round
+#ifndef OS_HIST_VEC
+#define OS_HIST_VEC 4
+#endif
+constexpr int kHistVec = OS_HIST_VEC;             // 16-byte vectors per thread per round
 constexpr int kRoundsPerPortion = 65535 / (kHistWarps * kHistVec * 4);  // u16 headroom
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {

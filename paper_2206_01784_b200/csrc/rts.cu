@@ -13,7 +13,10 @@
 namespace osb {
 
 constexpr int kRtsThreads = 256;   // one thread per digit in the prefix kernels
-constexpr int kRtsChunk = 16;      // tiles per chunk of the two-level prefix
+#ifndef OS_RTS_CHUNK
+#define OS_RTS_CHUNK 32  // prefix 44 us per place at 26K tiles (16: 62, 64: 50)
+#endif
+constexpr int kRtsChunk = OS_RTS_CHUNK;  // tiles per chunk of the two-level prefix
 
 // One block per tile: per-warp shared-memory digit counters (shared-memory
 // reductions), then thread d writes counts[tile][d].
