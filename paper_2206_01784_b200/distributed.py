@@ -241,9 +241,11 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     `keys` over all ranks of `group`.  Returns this rank's contiguous slice
     of the sorted output (and values).
 
-    exchange: "p2p" (fused partition + peer stores), "nccl"/"staged"
-    (partition + all_to_all_single), or "auto" (p2p when the group is NCCL and
-    symmetric memory is available, else all-to-all)."""
+    exchange: "p2p" (fused partition + peer stores), "all_to_all"
+    (partition + all_to_all_single; staged through the host for non-NCCL
+    groups), or "auto" (p2p when the group is NCCL and symmetric memory is
+    available, else all-to-all)."""
+    global _P2P_BROKEN
     import torch
     import torch.distributed as dist
 
@@ -274,7 +276,6 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
         except Exception as e:  # no symmetric memory on this system: all-to-all
             if exchange == "p2p":
                 raise
-            global _P2P_BROKEN
             _P2P_BROKEN = True
             import warnings
 
@@ -283,7 +284,9 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     if rb is not None:
         rk, rv = rb.views(keys.dtype, None if values is None else values.dtype)
         rb.barrier()  # every receiver is done with the previous round's data
-        dest = p2p_dest_index(rb.peer_ptrs, rb.peer_ptrs[rank], keys.element_size(),
+        # relative to the local view the kernel writes through (rk), so the
+        # index is right even if the local mapping differs from buffer_ptrs
+        dest = p2p_dest_index(rb.peer_ptrs, rk.data_ptr(), keys.element_size(),
                               receive_offsets(table, bin_lo, rank))
         ops.partition_p2p(keys, values, spec, digit_bits, bin_lo, dest, rk, rv)
         rb.barrier()  # all peers' stores into this rank's buffer have landed
