@@ -26,11 +26,16 @@
 //   5. write each run with coalesced stores at base + exclusive + (slot -
 //      start); the codec (signed/float decode) is applied on the way out.
 //
-// The pass is bound by the SM's shared-memory/L1 data pipe, not by HBM
-// (profiles/round1_ncu_summary.md): every digit-indexed table access by 32
-// random digits costs ~3 bank wavefronts.  The layout choices below trade
-// instructions for wavefronts: 16-bit per-warp counters (two digits per
-// bank word) and a 32-bit output-index table for the run writes.
+// Between ranking and reorder each thread parks its keys (and values) in its
+// own TMEM lane (tcgen05.st / tcgen05.ld), which frees the registers that
+// would hold them and lets four 10K-key tiles share an SM.
+//
+// The pass is SM-bound, not HBM-bound (profiles/round1_ncu_summary.md): the
+// ranking loop is issue/ALU-bound, the reorder and run writes are bound by
+// the shared-memory/L1 data pipe, where every digit-indexed table access by
+// 32 random digits costs ~3 bank wavefronts.  The layout choices below trade
+// instructions for wavefronts: 16-bit per-warp counters (two digits per bank
+// word) and a 32-bit output-index table for the run writes.
 //
 // Keys move once in and once out: 2n element transfers per pass, the
 // reference's ledger identity (binning.py:268-272).
@@ -631,9 +636,9 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
 }
 
 // Tile geometry per (key, value) width: THREADS x ITEMS keys per tile, MINB
-// resident blocks per SM.  Small blocks with many keys per thread keep four
-// tiles per SM in flight, which hides the TMA and look-back latencies of
-// each (measured in profiles/round1_binning_notes.md).
+// resident blocks per SM.  Small blocks with many keys per thread keep three
+// or four tiles per SM in flight, which hides the TMA and look-back latencies
+// of each (measured in profiles/round1_binning_notes.md).
 template <int KB, int VB> struct Geometry;
 #ifndef OS_U32_THREADS
 #define OS_U32_THREADS 256
@@ -653,7 +658,7 @@ template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2;
 #define OS_P32_B 3
 #endif
 #ifndef OS_K64_T
-// keys + values in TMEM: 256 x 32 at 2 blocks/SM, 1520 us/pass (C4, 20.7 GKey/s)
+// keys + values in TMEM: 256 x 32 at 2 blocks/SM, 1510 us/pass (C4, 20.8 GKey/s)
 // vs 256 x 16 at 3 blocks/SM without the stash, 1640 us/pass
 #define OS_K64_T 256
 #define OS_K64_I 32
