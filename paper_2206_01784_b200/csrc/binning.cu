@@ -89,6 +89,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #ifndef OS_STATUS_KEEP
 #define OS_STATUS_KEEP 0  // 1: status words carry an L2 evict_last policy (tools/gpu_status_l2.sh; 709 vs 707 us)
 #endif
+#ifndef OS_PDL
+#define OS_PDL 1  // binning passes use programmatic dependent launch (2.976 -> 2.947 ms per C2 sort)
+#endif
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
 #endif
@@ -180,7 +183,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       st_relaxed_gpu(a, v);
   };
 
+  if (OS_PDL) grid_launch_dependents();  // the next pass may start its prologue
   if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
+  // programmatic dependent launch: everything above overlaps the previous
+  // pass's tail; its output (this pass's input) is complete after the wait
+  if (OS_PDL) grid_dependency_wait();
   if (tid == 0) {
     const uint32_t t = atomicAdd(P.tile_counter, 1u);
     s_tile = t;
@@ -631,6 +638,19 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     configured = true;
   }
   if (p.num_tiles == 0) return cudaSuccess;
+  if (OS_PDL) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.num_tiles);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Smem::kBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+  }
   kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
   return cudaGetLastError();
 }

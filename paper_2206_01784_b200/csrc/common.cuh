@@ -404,6 +404,14 @@ __device__ __forceinline__ void tma_bulk_g2s_hint(void* dst_smem, const void* sr
       : "memory");
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---- launch descriptors ------------------------------------------------------
 struct PassParams {
   const void* src_keys;  // strip-relative base already applied by the host

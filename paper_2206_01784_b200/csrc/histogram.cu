@@ -203,6 +203,7 @@ constexpr size_t kHistU32Smem = 4 * 256 * 32 * 4;
 template <bool CODED>
 __global__ void __launch_bounds__(kHistThreads, 1)
     onesweep_histogram_u32d8_kernel(const HistParams P) {
+  grid_launch_dependents();  // lets a PDL-launched first pass start its prologue
   extern __shared__ uint32_t s_cnt[];  // [place][digit][lane]
   __shared__ unsigned long long s_wsum[kHistWarps];
   __shared__ bool s_last;
