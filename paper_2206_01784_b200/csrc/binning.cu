@@ -90,7 +90,7 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #define OS_STATUS_KEEP 0  // 1: status words carry an L2 evict_last policy (tools/gpu_status_l2.sh; 709 vs 707 us)
 #endif
 #ifndef OS_PDL
-#define OS_PDL 1  // binning passes use programmatic dependent launch (2.976 -> 2.947 ms per C2 sort)
+#define OS_PDL 0  // 1: programmatic dependent launch between passes (tools/size_sweep.py: no gain on plain sorts, -9 % at 16M keys)
 #endif
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
