@@ -22,6 +22,9 @@ namespace osb {
 
 constexpr int kHistThreads = 1024;
 constexpr int kHistWarps = kHistThreads / 32;
+#ifndef OS_HIST_L2PF
+#define OS_HIST_L2PF 0  // 1: histogram loads carry an L2 256-byte prefetch hint
+#endif
 #ifndef OS_HIST_VEC
 #define OS_HIST_VEC 4
 #endif
@@ -30,7 +33,11 @@ constexpr int kRoundsPerPortion = 65535 / (kHistWarps * kHistVec * 4);  // u16 h
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
   uint4 v;
+#if OS_HIST_L2PF
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
