@@ -166,6 +166,9 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     if to_numpy:
         keys = np.asarray(keys)
     spec = spec_for_dtype(keys.dtype)  # KeyError for unsupported dtypes
+    # without a config the tile is the device's own (its largest tile for the
+    # key/value widths); an explicit config's tile_size is honoured up to it
+    device_tile = cfg is None
     if cfg is None:
         cfg = radix_plan(spec.bits, 8)
     elif cfg.key_bits != spec.bits:
@@ -196,8 +199,8 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     ok = torch.empty_like(dk)
     ov = torch.empty_like(dv) if dv is not None else None
     d = _device_digit_bits(cfg)
-    sorter = DeviceSorter(n, dk.dtype, vb, d, begin_bit, end_bit, cfg.tile_size, cfg.strip_size,
-                          device=dk.device)
+    sorter = DeviceSorter(n, dk.dtype, vb, d, begin_bit, end_bit,
+                          0 if device_tile else cfg.tile_size, cfg.strip_size, device=dk.device)
     sorter(dk, ok, dv, ov, stream=stream if stream is not None else executor.stream)
     executor.ledger_record("histogram", "element_reads", n)
     executor.ledger_record("partition", "element_reads", sorter.passes * n)
