@@ -78,6 +78,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #endif
 
 // Skip the multisplit for warps whose 32*ITEMS keys share one digit.
+#ifndef OS_UNIFORM_KEYS
+#define OS_UNIFORM_KEYS 1  // keys-only passes take the uniform-warp shortcut too (tools/keys_dist.py)
+#endif
 #ifndef OS_UNIFORM_WARPS
 #define OS_UNIFORM_WARPS 1
 #endif
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // (key-value passes only: in the 64-register keys-only kernel the extra
   // code spills and costs the uniform-key case 2.6 %)
   bool uniform_warp = false;
-  if (OS_UNIFORM_WARPS && HAS_V && full) {
+  if (OS_UNIFORM_WARPS && (HAS_V || OS_UNIFORM_KEYS) && full) {
     const K xa = CODED ? cin(s_keys[warp_base + lane]) : s_keys[warp_base + lane];
     const K xb = CODED ? cin(s_keys[warp_base + (ITEMS - 1) * 32 + lane])
                        : s_keys[warp_base + (ITEMS - 1) * 32 + lane];
