@@ -73,7 +73,7 @@ The bench's live CUDA-event split agrees: histogram {b["kernels"]["histogram_us"
 ## Reading
 
 * **The binning pass is SM-bound, not HBM-bound.** It moves exactly its algorithmic bytes, at {b["roofline"]["frac"]*100:.0f} % of the measured copy bandwidth. Two SM resources take turns as the limiter. During ranking (46 % of a tile's ~13 µs life, `round1_trace.txt`) the SM is issue- and ALU-bound: ~35 instructions per 32 keys, four tiles ranking at once. In the reorder and run writes it is the shared-memory data pipe: {bi["smem_wavefronts"]/items:.1f} wavefronts per item over the whole kernel, half of them bank conflicts from 32 random digits.
-* **What this round changed.** Parking each thread's keys in TMEM (`tcgen05.st/ld`) between ranking and reorder freed the registers that held them. That allowed larger tiles and then a fourth tile per SM: 738 → 693 µs per pass, 69.7 → {bi["inst_executed"]/items:.1f} instructions per item, 18.4 → {bi["smem_wavefronts"]/items:.1f} shared wavefronts per item (`round1_binning_notes.md`, session 3).
+* **What this round changed.** Parking each thread's keys in TMEM (`tcgen05.st/ld`) between ranking and reorder freed the registers that held them. That allowed larger tiles and then a fourth tile per SM: 738 → {b["roofline"]["launch_us"]:.0f} µs per pass (with the later keys-only uniform-warp shortcut), 69.7 → {bi["inst_executed"]/items:.1f} instructions per item, 18.4 → {bi["smem_wavefronts"]/items:.1f} shared wavefronts per item (`round1_binning_notes.md`, session 3).
 * **What the rest of the time is.** With throwaway what-if builds, dropping the run writes saves 180 µs per pass. Sending the same writes to an L2-resident window still saves 140 µs, so the HBM write stream, and not SM work, is most of the output phase. The look-back costs little: the reduce-then-scan downsweep is this kernel without the look-back, and it takes 651 µs against 693 at 10K-key tiles (`round1_rts_ablation.md`). In the 16K-tile what-if, removing the look-back changed nothing.
 * **L2 hit rate of the look-back status words: ~90 %.** Measured by tagging every status load and store with an L2 evict_last policy. Nothing else in the kernels uses that policy, so the evict_last sector counters isolate the look-back traffic: `lts__t_sectors_srcunit_tex_evict_last_lookup_hit/miss` = 16.7 M / 1.47 M sectors per pass at 10K-key tiles, 91.9 %, i.e. ~580 MB of status traffic per pass, nearly all served by L2 (`tools/gpu_status_l2.sh`, `profiles/round1_status_l2.csv`, 4 launches). The misses are first touches of each tile's row. The policy itself is timing-neutral (709 vs 707 µs at 16K tiles), so the product build leaves it off (`OS_STATUS_KEEP`).
 * **Histogram.** HBM-bound at ~92 % of measured copy bandwidth (lane-private counters make every shared-memory add conflict-free).
