@@ -263,3 +263,25 @@ def test_sort_pipeline_matches_onesweep_sort(cuda):
     for (k, v), (ok, ov) in zip(ins, outs):
         wk, wv = onesweep_sort(k.numpy(), v.numpy())
         assert np.array_equal(ok.numpy(), wk) and np.array_equal(ov.numpy(), wv)
+
+
+@pytest.mark.parametrize("case", ["all-equal", "q16", "presorted", "two-digits"])
+def test_keys_only_uniform_warp_shortcut(cuda, case):
+    """Keys-only passes skip the multisplit for warps whose keys share one
+    digit (OS_UNIFORM_KEYS): the output must still be the stable sort, for
+    inputs where such warps are common, rare, or mixed within a tile."""
+    import torch
+
+    from paper_2206_01784_b200 import KeyGenSpec, generate_keys, onesweep_sort
+
+    n = (1 << 24) + 12345
+    if case == "all-equal":
+        keys = np.full(n, 0xABACADAE, dtype=np.uint32)
+    elif case == "q16":
+        keys = generate_keys(KeyGenSpec(q=16, seed=3, n=n), device="cuda").cpu().numpy()
+    elif case == "presorted":
+        keys = np.sort(generate_keys(KeyGenSpec(q=1, seed=4, n=n), device="cuda").cpu().numpy())
+    else:  # long runs of one value, then another: uniform and mixed warps
+        keys = np.where((np.arange(n) // 5000) % 2 == 0, 0x11223344, 0x11223345).astype(np.uint32)
+    got = onesweep_sort(torch.from_numpy(keys).cuda()).cpu().numpy()
+    assert np.array_equal(got, np.sort(keys, kind="stable"))
