@@ -81,3 +81,26 @@ def workspace(nbytes: int, device):
     import torch
 
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def launch_on(stream, tensors, launch) -> None:
+    """Run `launch(stream)` ordered against the current stream.
+
+    The inputs, outputs and workspace in `tensors` were allocated (and the
+    inputs uploaded) on the current stream.  When the caller names another
+    stream, that stream first waits for the current one, the tensors are
+    marked as used on it (so the caching allocator cannot hand them out while
+    the kernels still run), and the current stream then waits for the sort,
+    so a later read or download on it sees the result."""
+    import torch
+
+    cur = torch.cuda.current_stream()
+    if stream is None or stream == cur:
+        launch(cur)
+        return
+    stream.wait_stream(cur)
+    launch(stream)
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+    cur.wait_stream(stream)

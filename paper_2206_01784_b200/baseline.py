@@ -18,7 +18,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from ._device import as_device, from_device, is_tensor, workspace
+from ._device import as_device, from_device, is_tensor, launch_on, workspace
 from .executor import Executor
 from .keycodec import radix_plan, spec_for_dtype
 
@@ -90,7 +90,8 @@ def rts_sort(keys, values=None, cfg=None, executor: Executor | None = None):
     ok = torch.empty_like(dk)
     ov = torch.empty_like(dv) if dv is not None else None
     sorter = DeviceRtsSorter(n, dk.dtype, vb, device=dk.device)
-    sorter(dk, ok, dv, ov, stream=executor.stream)
+    launch_on(executor.stream, (dk, ok, dv, ov, sorter.ws),
+              lambda s: sorter(dk, ok, dv, ov, stream=s))
     for _ in range(sorter.passes):  # baseline.py:70,116-117
         executor.ledger_record("upsweep", "element_reads", n)
         executor.ledger_record("downsweep", "element_reads", n)

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from ._device import as_device, from_device, is_tensor, workspace
+from ._device import as_device, from_device, is_tensor, launch_on, workspace
 from .executor import Executor
 from .keycodec import MAX_DEVICE_DIGIT_BITS, RadixConfig, radix_plan, spec_for_dtype
 
@@ -201,7 +201,9 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     d = _device_digit_bits(cfg)
     sorter = DeviceSorter(n, dk.dtype, vb, d, begin_bit, end_bit,
                           0 if device_tile else cfg.tile_size, cfg.strip_size, device=dk.device)
-    sorter(dk, ok, dv, ov, stream=stream if stream is not None else executor.stream)
+    launch_on(stream if stream is not None else executor.stream,
+              (dk, ok, dv, ov, sorter.ws, sorter.stats),
+              lambda s: sorter(dk, ok, dv, ov, stream=s))
     executor.ledger_record("histogram", "element_reads", n)
     executor.ledger_record("partition", "element_reads", sorter.passes * n)
     executor.ledger_record("partition", "element_writes", sorter.passes * n)

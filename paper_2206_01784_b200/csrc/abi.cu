@@ -425,8 +425,22 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
   if (workspace == nullptr || workspace_bytes < L.total)
     return fail(OS_ERR_WORKSPACE, "sort workspace needs %zu bytes, got %zu", L.total,
                 workspace_bytes);
-  if (keys_out == keys_in && (L.passes % 2) == 1)
-    return fail(OS_ERR_ARG, "in-place sort needs an even pass count");
+  {
+    // Aliasing: with an odd pass count pass 0 writes the caller's output while
+    // other tiles still read the input, so no output may overlap any input.
+    // With an even count the inputs are dead after pass 0 and may be reused.
+    auto overlap = [](const void* a, size_t an, const void* b, size_t bn) {
+      const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+      return an != 0 && bn != 0 && x < y + bn && y < x + an;
+    };
+    const size_t kbytes = n * kb, vbytes = n * vb;
+    if (overlap(keys_out, kbytes, vals_out, vbytes))
+      return fail(OS_ERR_ARG, "keys_out and vals_out overlap");
+    if ((L.passes % 2) == 1 &&
+        (overlap(keys_out, kbytes, keys_in, kbytes) || overlap(keys_out, kbytes, vals_in, vbytes) ||
+         overlap(vals_out, vbytes, keys_in, kbytes) || overlap(vals_out, vbytes, vals_in, vbytes)))
+      return fail(OS_ERR_ARG, "in-place sort needs an even pass count");
+  }
   if (n > size_t(osb::histogram_grid_size()) * (size_t(1) << 31))
     return fail(OS_ERR_ARG, "n too large");
 
@@ -728,8 +742,13 @@ int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* 
     void* dst_k = to_out ? keys_out : tmp_k;
     void* dst_v = to_out ? vals_out : tmp_v;
     const int shift = 8 * k;
-    OS_CUDA(launch_rts_upsweep(src_k, n, kb, tile, shift, 0xffu, k == 0 ? kt.enc : CODEC_NONE,
-                               counts, s), "rts upsweep");
+    // upsweep tiled exactly like the downsweep: per strip, so that the count
+    // row of every downsweep tile is the one its upsweep tile wrote
+    for (size_t st = 0, tb = 0; st < L.t.strips; tb += L.t.strip_tiles(st), ++st)
+      OS_CUDA(launch_rts_upsweep(static_cast<const unsigned char*>(src_k) + st * L.t.strip * kb,
+                                 L.t.strip_len(st), kb, tile, shift, 0xffu,
+                                 k == 0 ? kt.enc : CODEC_NONE, counts + tb * kMaxRadix, s),
+              "rts upsweep");
     OS_CUDA(mark(1 + 3 * k), "event");
     OS_CUDA(launch_rts_prefix(counts, uint32_t(L.t.tiles_total), kMaxRadix, csum, offsets, s),
             "rts prefix");

@@ -71,8 +71,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 // are volatile, so they keep program order, and the warp is converged (no
 // divergent branches in the loop), so they also execute in order.
 // OS_SYNCWARP adds the formal __syncwarp() fences (bit 0: read -> leader write,
-// bit 1: leader write -> next read; one NOP each).  Timing: both 706 us,
-// bit 0 only 705, bit 1 only 710, none 707 (noise level); both are kept.
+// bit 1: leader write -> next read; one NOP each).  Timing (round 2, 10K
+// tiles, 3 interleaved runs): both 686 us, none 728; with the key prefetch
+// both 659, none 705 -- the NOPs pay for themselves in the warp schedule.
 #ifndef OS_SYNCWARP
 #define OS_SYNCWARP 3
 #endif
@@ -97,6 +98,9 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #endif
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
+#endif
+#ifndef OS_KEY_PREFETCH
+#define OS_KEY_PREFETCH 1  // 1: the ranking loop loads item i+1's key while ranking item i (659 vs 686 us/pass, C2)
 #endif
 
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   }
   if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+  asm volatile("" ::: "memory");  // the copies above before the (volatile) key loads below
   if (OS_TRACE && trace && tid == 0) trace[1] = global_ns();
 
   auto digit = [&](K x) -> uint32_t {  // x is an encoded key
@@ -334,10 +339,21 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     constexpr bool FULL = decltype(full_tag)::value;
     const uint32_t lt = lanemask_lt();
     const uint32_t le = lt | (1u << lane);
+    // next item's key, loaded one item ahead (volatile: issued before this
+    // item's counter read, so the load latency overlaps the ballots)
+    [[maybe_unused]] K xnext;
+    if (OS_KEY_PREFETCH) xnext = lds_key<K>(smem_base + (warp_base + lane) * KB);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
-      const K x = CODED ? cin(s_keys[idx]) : s_keys[idx];
+      K xraw;
+      if (OS_KEY_PREFETCH) {
+        xraw = xnext;
+        if (i + 1 < ITEMS) xnext = lds_key<K>(smem_base + (idx + 32) * KB);
+      } else {
+        xraw = s_keys[idx];
+      }
+      const K x = CODED ? cin(xraw) : xraw;
       if constexpr (STASH) stash_key(i, x);
       uint32_t d;
       if (FULL)
@@ -362,8 +378,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // ranks are the positions themselves.  Test cheaply first (first and last
   // item), then every item; uniform keys fail the first test at once, while
   // low-entropy and presorted inputs skip the ballots for most warps.
-  // (key-value passes only: in the 64-register keys-only kernel the extra
-  // code spills and costs the uniform-key case 2.6 %)
+  // Key-value passes always take it; keys-only passes take it when
+  // OS_UNIFORM_KEYS is set (the default: tools/keys_dist.py measured all-equal
+  // keys +21 % and uniform keys -1 % at 2^28, profiles/round1_binning_notes.md).
   bool uniform_warp = false;
   if (OS_UNIFORM_WARPS && (HAS_V || OS_UNIFORM_KEYS) && full) {
     const K xa = CODED ? cin(s_keys[warp_base + lane]) : s_keys[warp_base + lane];

@@ -170,6 +170,18 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
 }
+template <typename K>
+__device__ __forceinline__ K lds_key(uint32_t addr) {
+  if constexpr (sizeof(K) == 8) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return K(v);
+  } else {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return K(v);
+  }
+}
 template <typename T>
 __device__ __forceinline__ void sts_val(uint32_t addr, T v) {
   if constexpr (sizeof(T) == 8)

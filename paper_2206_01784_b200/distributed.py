@@ -221,6 +221,17 @@ def _symmetric_receive(need: int, elem_bytes: int, device, group):
 _P2P_BROKEN = False
 
 
+def _all_agree(ok: bool, device, group) -> bool:
+    """MIN all-reduce of a per-rank flag: True only if it holds on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    dev = device if dist.get_backend(group) == "nccl" else "cpu"
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(int(flag.item()) == 1)
+
+
 def _p2p_usable(keys, values, group) -> bool:
     import torch.distributed as dist
 
@@ -268,18 +279,29 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     send, recv = exchange_counts(table, bin_lo, rank)
 
     rb = None
-    if exchange in ("auto", "p2p") and (exchange == "p2p" or _p2p_usable(keys, values, group)):
+    want_p2p = exchange == "p2p" or (exchange == "auto" and _p2p_usable(keys, values, group))
+    if exchange == "auto":
+        # every rank must take the same path (the p2p barriers and the
+        # all-to-all are both collective), so the candidates agree first ...
+        want_p2p = _all_agree(want_p2p, keys.device, group)
+    if want_p2p:
         # capacity: the largest receive count of any rank (same on all ranks)
         need = max(int(table[:, bin_lo[g]:bin_lo[g + 1]].sum()) for g in range(world))
+        err = None
         try:
             rb = _symmetric_receive(need, keys.element_size(), keys.device, group)
-        except Exception as e:  # no symmetric memory on this system: all-to-all
+        except Exception as e:  # noqa: BLE001 -- no symmetric memory here
+            err = e
+        # ... and so does the outcome of the setup: a rank whose allocation or
+        # rendezvous failed must not leave the others waiting in a barrier
+        if not _all_agree(err is None, keys.device, group):
+            rb = None
             if exchange == "p2p":
-                raise
-            _P2P_BROKEN = True
+                raise RuntimeError(f"p2p exchange setup failed on some rank ({err})")
+            _P2P_BROKEN = True  # sticky, and the same decision on every rank
             import warnings
 
-            warnings.warn(f"p2p exchange unavailable ({e}); using all_to_all")
+            warnings.warn(f"p2p exchange unavailable ({err or 'failed on a peer'}); using all_to_all")
     exchange = "p2p" if rb is not None else "all_to_all"
     if rb is not None:
         rk, rv = rb.views(keys.dtype, None if values is None else values.dtype)
@@ -342,6 +364,31 @@ def emulate_p2p_sort(shards, value_shards=None, *, ops=None, digit_bits: int = S
     return out, {"bin_lo": bin_lo, "recv": recv}
 
 
+def _peer_mapping_ok(device, group) -> bool:
+    """Each rank writes a rank-tagged token into every peer's symmetric
+    buffer through the peer mapping; after a stream sync and a host-side
+    barrier (the process group's own timeout applies) each rank checks that
+    all tokens arrived.  False on any failure."""
+    import torch
+    import torch.distributed as dist
+
+    try:
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        rb = _symmetric_receive(world, 8, device, group)
+        for g in range(world):
+            peer = rb.handle.get_buffer(g, (world,), torch.int64)
+            peer[rank: rank + 1].fill_(0x5EED0000 + rank)
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+        mine = rb.handle.get_buffer(rank, (world,), torch.int64).cpu()
+        want = torch.arange(world, dtype=torch.int64) + 0x5EED0000
+        ok = bool(torch.equal(mine, want))
+        dist.barrier(group=group)  # nobody reuses the buffer before every check
+        return ok
+    except Exception:  # noqa: BLE001
+        return False
+
+
 class ShardedSorter:
     """Bench helper: a sharded sort of `n` keys per rank.
 
@@ -374,6 +421,12 @@ class ShardedSorter:
             k.to(dev).to(key_dtype)
         ok = 1
         try:
+            # first a host-checked store through every peer mapping (plain
+            # copies, no device-side barrier that could spin forever), agreed
+            # by all ranks before anything waits on a peer
+            ok = int(_all_agree(_peer_mapping_ok(dev, self.group), dev, self.group))
+            if not ok:
+                raise RuntimeError("peer mapping check failed")
             a = sharded_sort(k, None, self.group, exchange="p2p")
             b = sharded_sort(k, None, self.group, exchange="all_to_all")
             ok = int(a.numel() == b.numel() and bool(torch.equal(a, b)))
