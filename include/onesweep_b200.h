@@ -71,6 +71,12 @@ typedef struct os_device_stats {
 const char* os_version(void);
 const char* os_last_error(void);
 
+/* Synchronise `stream` (NULL: the whole device) and report any asynchronous kernel fault (a trapped
+ * look-back watchdog, an illegal address) as OS_ERR_CUDA with its message.
+ * Calls are asynchronous; this is the debug-mode check after each call
+ * (the Python layer runs it when ONESWEEP_B200_SYNC_CHECK=1). */
+int os_stream_check(void* stream);
+
 /* Largest digit width the binning kernel supports natively (radix <= 256). */
 int os_max_digit_bits(void);
 
@@ -94,7 +100,8 @@ int os_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
  * [begin_bit, end_bit) of the *encoded* key (codec applied on load).
  * hist_out:    u64[passes][radix], overwritten (not accumulated).
  * offsets_out: u64[passes][radix] exclusive sums per place, or NULL.
- * passes = ceil((end_bit - begin_bit) / digit_bits).
+ * passes = ceil((end_bit - begin_bit) / digit_bits); digit_bits in [1, 16]
+ * (the reference's range, keycodec.py:110; widths > 8 take the wide kernel).
  * workspace:   os_histogram_workspace_bytes() bytes (zeroed by the call). */
 size_t os_histogram_workspace_bytes(void);
 int os_histogram(const void* keys, size_t n, int key_bytes, int codec, int digit_bits,
@@ -120,10 +127,17 @@ int os_exclusive_scan(const unsigned long long* counts, int rows, int radix,
  * status_out: optional device u32 buffer of os_partition_status_words()
  *             words that receives the final status words of every strip
  *             (tile-major, strips concatenated); NULL = internal.
- * workspace: os_partition_workspace_bytes() bytes. */
+ * digit_width in [1, 16].  Widths 9..16 run as two stable <= 8-bit binning
+ * launches into scratch plus a scatter to base[d] + rank (csrc/wide.cu); they
+ * need codec_in in {NONE, SIGNED, FLOAT_ENC}, keep no status words
+ * (status_out must be NULL) and do not update stats.
+ * workspace: os_partition_workspace_bytes_kv() bytes (for widths <= 8 this
+ * equals os_partition_workspace_bytes(), which cannot size widths > 8). */
 size_t os_partition_status_words(size_t n, int digit_width, int tile_keys, size_t strip_keys);
 size_t os_partition_workspace_bytes(size_t n, int digit_width, int tile_keys,
                                     size_t strip_keys);
+size_t os_partition_workspace_bytes_kv(size_t n, int key_bytes, int val_bytes, int digit_width,
+                                       int tile_keys, size_t strip_keys);
 int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals,
                       void* dst_vals, size_t n, int key_bytes, int val_bytes, int shift,
                       int digit_width, const unsigned long long* base_offsets,

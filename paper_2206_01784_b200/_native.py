@@ -35,6 +35,7 @@ SIGNATURES = {
     "os_version": (ctypes.c_char_p, []),
     "os_last_error": (ctypes.c_char_p, []),
     "os_max_digit_bits": (_i, []),
+    "os_stream_check": (_i, [_vp]),
     "os_tile_capacity": (_i, [_i, _i]),
     "os_encode": (_i, [_vp, _vp, _sz, _i, _vp]),
     "os_decode": (_i, [_vp, _vp, _sz, _i, _vp]),
@@ -44,6 +45,7 @@ SIGNATURES = {
     "os_exclusive_scan": (_i, [_vp, _i, _i, _vp, _vp]),
     "os_partition_status_words": (_sz, [_sz, _i, _i, _sz]),
     "os_partition_workspace_bytes": (_sz, [_sz, _i, _i, _sz]),
+    "os_partition_workspace_bytes_kv": (_sz, [_sz, _i, _i, _i, _i, _sz]),
     "os_partition_pass": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _sz,
                                _vp, _vp, _sz, _vp, _vp]),
     "os_sort_workspace_bytes": (_sz, [_sz, _i, _i, _i, _i, _i, _i, _sz]),
@@ -88,8 +90,17 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+# ONESWEEP_B200_SYNC_CHECK=1: after every successful call, synchronise the
+# device and raise on an asynchronous kernel fault at the call that caused it
+# (debug mode; calls are otherwise asynchronous on their stream).
+SYNC_CHECK = os.environ.get("ONESWEEP_B200_SYNC_CHECK", "0") not in ("", "0")
+
+
 def check(rc: int, what: str = "") -> None:
     """Map an os_status onto the reference's exception classes."""
+    if rc == OS_OK and SYNC_CHECK:
+        rc = load().os_stream_check(None)  # NULL stream: legacy default, waits for all
+        what = f"{what} (asynchronous)" if what else "asynchronous"
     if rc == OS_OK:
         return
     msg = load().os_last_error().decode(errors="replace")

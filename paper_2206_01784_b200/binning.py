@@ -204,9 +204,16 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     launch_on(stream if stream is not None else executor.stream,
               (dk, ok, dv, ov, sorter.ws, sorter.stats),
               lambda s: sorter(dk, ok, dv, ov, stream=s))
+    # The ledger is the algorithmic traffic of the configured plan, as the
+    # reference defines it (binning.py:268-272, executor.py:10-14): one read
+    # for the histogram, one read and one write per cfg.digit_bits place.
+    # For cfg.digit_bits > 8 the device runs 8-bit places (same output); its
+    # own element moves are in executor.device_element_ops.
+    plan_passes = -(-(end_bit - begin_bit) // cfg.digit_bits)
     executor.ledger_record("histogram", "element_reads", n)
-    executor.ledger_record("partition", "element_reads", sorter.passes * n)
-    executor.ledger_record("partition", "element_writes", sorter.passes * n)
+    executor.ledger_record("partition", "element_reads", plan_passes * n)
+    executor.ledger_record("partition", "element_writes", plan_passes * n)
+    executor.device_element_ops += (1 + 2 * sorter.passes) * n
     executor.record_device_stats("partition", sorter.stats, 1 << d)
     sk = from_device(ok, to_numpy)
     if values is None:
@@ -229,8 +236,8 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
 
     from .lookback import CounterMatrix
 
-    if cfg.digit_bits > MAX_DEVICE_DIGIT_BITS:
-        raise ValueError(f"device passes bin at most {MAX_DEVICE_DIGIT_BITS} bits per place")
+    if return_status and cfg.digit_bits > MAX_DEVICE_DIGIT_BITS:
+        raise ValueError(f"status words are only kept for digit_bits <= {MAX_DEVICE_DIGIT_BITS}")
     executor = executor or Executor()
     shift = cfg.digit_shift(place)
     src_np = not is_tensor(src_keys)
@@ -255,7 +262,8 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
     n = sk.numel()
     cap = L.os_tile_capacity(cfg.key_bits // 8, vb)
     tile = min(cfg.tile_size, cap)
-    ws = workspace(L.os_partition_workspace_bytes(n, cfg.digit_bits, tile, cfg.strip_size), sk.device)
+    ws = workspace(L.os_partition_workspace_bytes_kv(n, cfg.key_bits // 8, vb, cfg.digit_bits, tile,
+                                                     cfg.strip_size), sk.device)
     status = None
     if return_status:
         words = L.os_partition_status_words(n, cfg.digit_bits, tile, cfg.strip_size)

@@ -144,6 +144,18 @@ uint32_t prefetch_tiles() {
   return uint32_t(v);
 }
 
+// Failure injection for the watchdog test (honoured by OS_JITTER builds
+// only): ONESWEEP_B200_DEBUG_STALL_TILE=t makes tile t of every pass skip its
+// status publishes, so its successors' look-backs must trap, not hang.
+int debug_stall_tile() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("ONESWEEP_B200_DEBUG_STALL_TILE");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
 // Diagnostics (os_debug_trace): per-tile timeline of one pass.
 unsigned long long* g_trace = nullptr;
 int g_trace_pass = -1;
@@ -192,6 +204,7 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     // (partition_pass callers may pass any base offsets)
     p.wide_index = !dense_bases || t.n >= (size_t(1) << 32) - (size_t(1) << 26);
     p.trace = trace ? trace + tile_base * kTraceWords : nullptr;
+    p.debug_stall_tile = debug_stall_tile();
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
     tile_base += p.num_tiles;
@@ -199,11 +212,12 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
   return OS_OK;
 }
 
-int check_bits(int key_bytes, int digit_bits, int begin_bit, int end_bit) {
+int check_bits(int key_bytes, int digit_bits, int begin_bit, int end_bit,
+               int max_bits = kMaxDigitBits) {
   const int kbits = key_bytes * 8;
-  if (digit_bits < 1 || digit_bits > kMaxDigitBits)
+  if (digit_bits < 1 || digit_bits > max_bits)
     return fail(OS_ERR_ARG, "digit_bits must be in [1, %d] on the device path, got %d",
-                kMaxDigitBits, digit_bits);
+                max_bits, digit_bits);
   if (begin_bit < 0 || end_bit > kbits || begin_bit >= end_bit)
     return fail(OS_ERR_ARG, "need 0 <= begin_bit < end_bit <= %d, got [%d, %d)", kbits,
                 begin_bit, end_bit);
@@ -249,7 +263,22 @@ SortLayout sort_layout(size_t n, int kb, int vb, int digit_bits, int begin_bit, 
 
 extern "C" {
 
-const char* os_version(void) { return "onesweep_b200 0.1.0 (sm_100a)"; }
+const char* os_version(void) {
+#if OS_JITTER
+  return "onesweep_b200 0.2.0 (sm_100a, debug: look-back jitter + failure injection)";
+#else
+  return "onesweep_b200 0.2.0 (sm_100a)";
+#endif
+}
+
+int os_stream_check(void* stream) {
+  // surfaces asynchronous kernel faults (a trapped look-back watchdog, an
+  // illegal address) at the call that caused them
+  OS_CUDA(stream ? cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) : cudaDeviceSynchronize(),
+          "asynchronous kernel error");
+  OS_CUDA(cudaGetLastError(), "asynchronous kernel error");
+  return OS_OK;
+}
 const char* os_last_error(void) { return g_err; }
 int os_max_digit_bits(void) { return kMaxDigitBits; }
 int os_tile_capacity(int key_bytes, int val_bytes) {
@@ -289,7 +318,7 @@ int os_histogram(const void* keys, size_t n, int key_bytes, int codec, int digit
                  unsigned long long* offsets_out, void* workspace, size_t workspace_bytes,
                  void* stream) {
   if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
-  if (int rc = check_bits(key_bytes, digit_bits, begin_bit, end_bit)) return rc;
+  if (int rc = check_bits(key_bytes, digit_bits, begin_bit, end_bit, kMaxWideDigitBits)) return rc;
   if (codec < CODEC_NONE || codec > CODEC_FLOAT_ENC)
     return fail(OS_ERR_ARG, "histogram codec must be NONE, SIGNED or FLOAT_ENC");
   if (workspace_bytes < os_histogram_workspace_bytes() || workspace == nullptr)
@@ -314,6 +343,13 @@ int os_histogram(const void* keys, size_t n, int key_bytes, int codec, int digit
   p.done_counter = static_cast<unsigned int*>(workspace);
   if (n == 0) {
     if (offsets_out) OS_CUDA(cudaMemsetAsync(offsets_out, 0, size_t(passes) * radix * 8, s), "memset");
+    return OS_OK;
+  }
+  if (digit_bits > kMaxDigitBits) {  // 2^9..2^16-way places (csrc/wide.cu)
+    OS_CUDA(launch_wide_histogram(keys, n, key_bytes, codec, begin_bit, digit_bits, passes,
+                                  p.top_bits, hist_out, s), "wide histogram launch");
+    if (offsets_out)
+      OS_CUDA(launch_exclusive_scan(hist_out, passes, radix, offsets_out, s), "exclusive scan");
     return OS_OK;
   }
   OS_CUDA(launch_histogram(p, key_bytes, s), "histogram launch");
@@ -342,6 +378,121 @@ size_t os_partition_workspace_bytes(size_t n, int digit_width, int tile_keys, si
   return pass_ws(t, 1 << digit_width, true).bytes;
 }
 
+}  // extern "C"
+
+namespace {
+// Scratch of a 2^9..2^16-way partition pass (csrc/wide.cu): two dense
+// ping-pong copies, the 8-bit sub-pass tables and the 2^d-way tables, then
+// the workspace of the 8-bit binning sub-passes.
+struct WideLayout {
+  Tiling t;
+  PassWs pw;
+  size_t off_ak = 0, off_av = 0, off_bk = 0, off_bv = 0, off_h8 = 0, off_o8 = 0, off_done = 0,
+         off_hw = 0, off_ow = 0, off_rel = 0, off_sub = 0, total = 0;
+};
+WideLayout wide_layout(size_t n, int kb, int vb, int width, uint32_t tile, size_t strip) {
+  WideLayout L;
+  L.t = make_tiling(n, tile, strip);
+  L.pw = pass_ws(L.t, kMaxRadix, true);
+  const size_t rw = size_t(1) << width;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off = align_up(off + bytes); return o; };
+  L.off_ak = take(n * kb);
+  L.off_av = take(n * vb);
+  L.off_bk = take(n * kb);
+  L.off_bv = take(n * vb);
+  L.off_h8 = take(2 * kMaxRadix * 8);
+  L.off_o8 = take(2 * kMaxRadix * 8);
+  L.off_done = take(kAlign);
+  L.off_hw = take(rw * 8);
+  L.off_ow = take(rw * 8);
+  L.off_rel = take(rw * 8);
+  L.off_sub = take(L.pw.bytes);
+  L.total = off;
+  return L;
+}
+
+int wide_partition(const void* src_k, void* dst_k, const void* src_v, void* dst_v, size_t n,
+                   int kb, int vb, int shift, int width, const unsigned long long* base,
+                   unsigned long long* carry_out, int codec_in, int codec_out, uint32_t tile,
+                   size_t strip, unsigned char* ws, size_t ws_bytes, cudaStream_t s) {
+  if (codec_in > CODEC_FLOAT_ENC)
+    return fail(OS_ERR_ARG, "codec_in must be NONE, SIGNED or FLOAT_ENC for digit widths > 8");
+  // the top place may reach past the key: its digit is zero-extended
+  // (keycodec.py:125-128), so only the bits inside the key are binned
+  const int kbits = kb * 8;
+  const int lo_w = kbits - shift < kMaxDigitBits ? kbits - shift : kMaxDigitBits;
+  const int hi_w = (width < kbits - shift ? width : kbits - shift) - lo_w;
+  const WideLayout L = wide_layout(n, kb, vb, width, tile, strip);
+  if (ws == nullptr || ws_bytes < L.total)
+    return fail(OS_ERR_WORKSPACE, "partition workspace needs %zu bytes, got %zu", L.total, ws_bytes);
+  const int radix = 1 << width;
+  auto u64 = [&](size_t off) { return reinterpret_cast<unsigned long long*>(ws + off); };
+  // 1. dense offsets of the digit's low byte and high (width - 8) bits
+  OS_CUDA(cudaMemsetAsync(ws + L.off_h8, 0, 2 * kMaxRadix * 8, s), "memset");
+  OS_CUDA(cudaMemsetAsync(ws + L.off_done, 0, kAlign, s), "memset");
+  HistParams hp{};
+  hp.keys = src_k;
+  hp.n = n;
+  hp.codec = codec_in;
+  hp.begin_bit = shift;
+  hp.digit_bits = kMaxDigitBits;
+  hp.passes = hi_w > 0 ? 2 : 1;
+  hp.top_bits = hi_w > 0 ? hi_w : lo_w;
+  hp.hist = u64(L.off_h8);
+  hp.offsets = u64(L.off_o8);
+  hp.done_counter = reinterpret_cast<unsigned int*>(ws + L.off_done);
+  OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  // 2.-3. two stable binning sub-passes: low byte, then the high bits
+  unsigned char* sub = ws + L.off_sub;
+  uint32_t* status = reinterpret_cast<uint32_t*>(sub + L.pw.off_status);
+  unsigned long long* scratch_carry = u64(L.off_rel);  // overwritten in step 5
+  void* ak = ws + L.off_ak;
+  void* av = vb ? ws + L.off_av : nullptr;
+  void* bk = ws + L.off_bk;
+  void* bv = vb ? ws + L.off_bv : nullptr;
+  OS_CUDA(cudaMemsetAsync(sub, 0, L.pw.zero_bytes, s), "memset");
+  if (int rc = run_pass(src_k, ak, src_v, av, kb, vb, L.t, shift, lo_w, kMaxRadix, nullptr,
+                        u64(L.off_o8), scratch_carry, codec_in, CODEC_NONE, status, nullptr, sub,
+                        L.pw, nullptr, s, /*dense_bases=*/true))
+    return rc;
+  if (hi_w > 0) {
+    OS_CUDA(cudaMemsetAsync(sub, 0, L.pw.zero_bytes, s), "memset");
+    if (int rc = run_pass(ak, bk, av, bv, kb, vb, L.t, shift + kMaxDigitBits, hi_w, kMaxRadix,
+                          nullptr, u64(L.off_o8) + kMaxRadix, scratch_carry, CODEC_NONE, CODEC_NONE,
+                          status, nullptr, sub, L.pw, nullptr, s, /*dense_bases=*/true))
+      return rc;
+  } else {  // the digit's high part lies past the key: the low sub-pass is the order
+    bk = ak;
+    bv = av;
+  }
+  // 4. dense starts of the full 2^width-way digit
+  OS_CUDA(cudaMemsetAsync(ws + L.off_hw, 0, size_t(radix) * 8, s), "memset");
+  OS_CUDA(launch_wide_histogram(bk, n, kb, CODEC_NONE, shift, width, 1, lo_w + hi_w, u64(L.off_hw),
+                                s), "wide histogram launch");
+  OS_CUDA(launch_exclusive_scan(u64(L.off_hw), 1, radix, u64(L.off_ow), s), "exclusive scan");
+  // 5. rel = base - dense start, carry = base + count; 6. scatter to dst
+  OS_CUDA(launch_wide_tables(base, u64(L.off_hw), u64(L.off_ow), radix, u64(L.off_rel), carry_out, s),
+          "wide tables");
+  OS_CUDA(launch_wide_scatter(bk, dst_k, bv, dst_v, kb, vb, n, shift, lo_w + hi_w, u64(L.off_rel),
+                              codec_out, s), "wide scatter");
+  return OS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t os_partition_workspace_bytes_kv(size_t n, int key_bytes, int val_bytes, int digit_width,
+                                       int tile_keys, size_t strip_keys) {
+  if (digit_width <= kMaxDigitBits)
+    return os_partition_workspace_bytes(n, digit_width, tile_keys, strip_keys);
+  if (digit_width > kMaxWideDigitBits || tile_keys <= 0 || (key_bytes != 4 && key_bytes != 8) ||
+      !valid_val_bytes(val_bytes))
+    return 0;
+  size_t strip = strip_keys ? strip_keys : kMaxStripKeys;
+  return wide_layout(n, key_bytes, val_bytes, digit_width, uint32_t(tile_keys), strip).total;
+}
+
 int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals, void* dst_vals,
                       size_t n, int key_bytes, int val_bytes, int shift, int digit_width,
                       const unsigned long long* base_offsets, unsigned long long* carry_out,
@@ -352,8 +503,8 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
   if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
   if ((val_bytes == 0) != (src_vals == nullptr) || (val_bytes == 0) != (dst_vals == nullptr))
     return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
-  if (digit_width < 1 || digit_width > kMaxDigitBits)
-    return fail(OS_ERR_ARG, "digit width must be in [1, %d]", kMaxDigitBits);
+  if (digit_width < 1 || digit_width > kMaxWideDigitBits)
+    return fail(OS_ERR_ARG, "digit width must be in [1, %d]", kMaxWideDigitBits);
   if (shift < 0 || shift >= key_bytes * 8) return fail(OS_ERR_ARG, "shift out of range");
   if (codec_in < 0 || codec_in > 3 || codec_out < 0 || codec_out > 3)
     return fail(OS_ERR_ARG, "bad codec");
@@ -361,6 +512,19 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
   if (int rc = resolve_tile(tile_keys, key_bytes, val_bytes, &tile)) return rc;
   size_t strip;
   if (int rc = resolve_strip(strip_keys, &strip)) return rc;
+  if (digit_width > kMaxDigitBits) {
+    if (status_out != nullptr)
+      return fail(OS_ERR_ARG, "status words are only kept for digit widths <= %d", kMaxDigitBits);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+      OS_CUDA(cudaMemcpyAsync(carry_out, base_offsets, (size_t(1) << digit_width) * 8,
+                              cudaMemcpyDeviceToDevice, s), "carry copy");
+      return OS_OK;
+    }
+    return wide_partition(src_keys, dst_keys, src_vals, dst_vals, n, key_bytes, val_bytes, shift,
+                          digit_width, base_offsets, carry_out, codec_in, codec_out, tile, strip,
+                          static_cast<unsigned char*>(workspace), workspace_bytes, s);
+  }
   const int radix = 1 << digit_width;
   Tiling t = make_tiling(n, tile, strip);
   PassWs w = pass_ws(t, radix, true);

@@ -99,8 +99,44 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 #ifndef OS_STASH64
 #define OS_STASH64 1  // 1: 64-bit keys are stashed in TMEM too (2 columns per key)
 #endif
+// Race exploration (the reference's Jitter, executor.py:108-121, applied
+// between publish and look-back at binning.py:187-193): OS_JITTER=1 debug
+// builds sleep a pseudo-random 0..OS_JITTER_NS ns (hash of tile, digit and
+// a per-build seed) before the L publish, before the look-back and before
+// the G publish, so tiles publish out of order and look-backs meet N words.
+#ifndef OS_JITTER
+#define OS_JITTER 0
+#endif
+#ifndef OS_JITTER_NS
+#define OS_JITTER_NS 20000
+#endif
+#ifndef OS_JITTER_SEED
+#define OS_JITTER_SEED 0x9E3779B9u
+#endif
+// Failure detection (the reference's aborting waiters, lookback.py:176-189):
+// a look-back that re-polls one unpublished predecessor word more than
+// OS_SPIN_LIMIT times traps (the launch fails with cudaErrorLaunchFailure /
+// illegal instruction) instead of hanging the GPU.  A healthy pass waits a
+// few microseconds; 2^26 re-polls is over a minute of L2 round trips.
+#ifndef OS_SPIN_LIMIT
+#define OS_SPIN_LIMIT (1u << 26)
+#endif
+__device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, uint32_t site) {
+  if (OS_JITTER) {
+    uint32_t h = tile * 0x9E3779B1u ^ (lane_id + 0x7F4A7C15u) * 0x85EBCA6Bu ^ site * 0xC2B2AE35u ^
+                 uint32_t(OS_JITTER_SEED);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 3u) != 0u) __nanosleep(h % uint32_t(OS_JITTER_NS));  // 3 in 4 threads sleep
+  }
+}
+
+#ifndef OS_RANK_STASH
+#define OS_RANK_STASH 0  // 1: keys-only passes park the packed ranks in TMEM too
+#endif
 #ifndef OS_KEY_PREFETCH
-#define OS_KEY_PREFETCH 1  // 1: the ranking loop loads item i+1's key while ranking item i (659 vs 686 us/pass, C2)
+#define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
 
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
@@ -140,7 +176,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
                          (!HAS_V || VB == 4) && ITEMS % 8 == 0 && WARPS % 4 == 0;
   constexpr int KW = KB / 4;                 // TMEM words per key
   constexpr int NW = KW + (HAS_V ? 1 : 0);   // stashed words per item: key (+ value)
-  constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * ITEMS * NW;
+  // packed ranks (two u16 per word) parked next to the keys, 4 words per store
+  constexpr bool RSTASH = OS_RANK_STASH && STASH && !HAS_V && KW == 1 && ITEMS % 8 == 0;
+  constexpr int RW = RSTASH ? ITEMS / 2 : 0;
+  constexpr uint32_t TCOLS_RAW = uint32_t(WARPS / 4) * (ITEMS * NW + RW);
   constexpr uint32_t TCOLS = TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64 : TCOLS_RAW <= 128 ? 128
                            : TCOLS_RAW <= 256 ? 256 : 512;
 
@@ -230,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   uint32_t taddr = 0;
   if (STASH) {
     tmem_fence_after_sync();
-    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * (ITEMS * NW);
+    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * (ITEMS * NW + RW);
   }
 
   const uint32_t tile = s_tile;
@@ -333,7 +372,26 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       return K(uint64_t(kc[2 * (i & 3)]) | (uint64_t(kc[2 * (i & 3) + 1]) << 32));
     }
   };
-  uint32_t ranks[(ITEMS + 1) / 2];  // two u16 scaled ranks per register
+  uint32_t ranks[RSTASH ? 4 : (ITEMS + 1) / 2];  // two u16 scaled ranks per register
+  const uint32_t rbase = taddr + uint32_t(ITEMS * NW);  // rank columns (RSTASH)
+  // rank of item i: even items in the low half-word, odd items in the high
+  auto put_rank = [&](int i, uint32_t rank) {
+    const int w = RSTASH ? (i / 2) & 3 : i / 2;
+    if (i & 1)
+      ranks[w] = fma_u32(rank, k_shl16, ranks[w]);
+    else
+      ranks[w] = rank;
+    if constexpr (RSTASH) {
+      if ((i & 7) == 7 || i == ITEMS - 1) tmem_st4(rbase + uint32_t((i / 8) * 4), ranks);
+    }
+  };
+  auto get_rank = [&](int i) -> uint32_t {
+    if constexpr (RSTASH) {
+      if ((i & 7) == 0) tmem_ld4(rbase + uint32_t((i / 8) * 4), ranks);
+    }
+    const int w = RSTASH ? (i / 2) & 3 : i / 2;
+    return (i & 1) ? (ranks[w] >> 16) : (ranks[w] & 0xffffu);
+  };
   const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
   auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
@@ -341,15 +399,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     const uint32_t le = lt | (1u << lane);
     // next item's key, loaded one item ahead (volatile: issued before this
     // item's counter read, so the load latency overlaps the ballots)
-    [[maybe_unused]] K xnext;
-    if (OS_KEY_PREFETCH) xnext = lds_key<K>(smem_base + (warp_base + lane) * KB);
+    constexpr int PF = OS_KEY_PREFETCH > 0 ? OS_KEY_PREFETCH : 1;
+    [[maybe_unused]] K xq[PF];
+    if (OS_KEY_PREFETCH) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j) xq[j] = lds_key<K>(smem_base + (warp_base + j * 32 + lane) * KB);
+    }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t idx = warp_base + i * 32 + lane;
       K xraw;
       if (OS_KEY_PREFETCH) {
-        xraw = xnext;
-        if (i + 1 < ITEMS) xnext = lds_key<K>(smem_base + (idx + 32) * KB);
+        xraw = xq[i % PF];
+        if (i + PF < ITEMS) xq[i % PF] = lds_key<K>(smem_base + (idx + 32 * PF) * KB);
       } else {
         xraw = s_keys[idx];
       }
@@ -365,10 +427,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       match_rank8(d, le, ~le, &upto, &leader);
       const uint32_t caddr = fma_u32(d, k_two, hbase);
       const uint32_t rank = lds_u16(caddr) + __popc(upto) * KB;
-      if (i & 1)
-        ranks[i / 2] = fma_u32(rank, k_shl16, ranks[i / 2]);
-      else
-        ranks[i / 2] = rank;
+      put_rank(i, rank);
       if (OS_SYNCWARP & 1) __syncwarp();
       if (leader) sts_u16(caddr, rank);
       if (OS_SYNCWARP & 2) __syncwarp();
@@ -397,9 +456,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       uniform_warp = __all_sync(0xffffffffu, same);
       if (uniform_warp) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; i += 2)
-          ranks[i / 2] = uint32_t(i * 32 + lane + 1) * KB |
-                         (i + 1 < ITEMS ? uint32_t((i + 1) * 32 + lane + 1) * KB << 16 : 0u);
+        for (int i = 0; i < ITEMS; ++i) put_rank(i, uint32_t(i * 32 + lane + 1) * KB);
         if (lane == 0) sts_u16(hbase + d0 * 2u, uint32_t(ITEMS * 32 * KB));
         if constexpr (STASH) {  // the keys still go to the stash
 #pragma unroll
@@ -429,6 +486,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
     if (P.rts_offsets == nullptr)  // (reduce-then-scan passes have no look-back)
+      if (OS_JITTER) jitter_sleep(tile, tid, 1);
+      if (!OS_JITTER || int(tile) != P.debug_stall_tile)
       status_st(P.status + size_t(tile) * radix + tid,
                 (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
     if (count == valid) s_fast = tid;
@@ -501,8 +560,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           key = unstash_key(i);
         else
           key = keys[i];
+        const uint32_t r = get_rank(i);  // (a warp-collective TMEM load under RSTASH)
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
-        const uint32_t r = (i & 1) ? (ranks[i / 2] >> 16) : (ranks[i / 2] & 0xffffu);
         const uint32_t off = lds_u16(fma_u32(digit(key), k_two, hbase));
         const uint32_t addr = fma_u32(off, k_one, fma_u32(r, k_one, slot0));
         sts_val(addr, key);
@@ -529,7 +588,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (tid < radix) {
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
+    if (OS_JITTER) jitter_sleep(tile, tid, 2);
     if (tile > 0 && P.rts_offsets == nullptr) {
+      uint32_t spins = 0;
       // p walks down the digit's column; 8-bit places have a compile-time row
       // stride, so the window's loads are one base register plus immediates
       const size_t stride = BYTE ? size_t(kMaxRadix) : size_t(radix);
@@ -554,6 +615,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           const uint32_t st = w[k] >> kStatusShift;
           if (st == 0u) {  // predecessor in flight: re-poll from here
             ++waits;
+            if (++spins > OS_SPIN_LIMIT) {
+              printf("onesweep: look-back stalled (tile %u digit %d waits on tile %d)\n", tile, tid,
+                     j - k);
+              __trap();
+            }
             break;
           }
           excl += w[k] & kValueMask;
@@ -565,7 +631,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         j -= k;
         p -= k * stride;
       }
-      status_st(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
+      if (OS_JITTER) jitter_sleep(tile, tid, 3);
+      if (!OS_JITTER || int(tile) != P.debug_stall_tile)
+        status_st(P.status + size_t(tile) * radix + tid, kFlagGlobal | (excl + count));
     }
     if (OS_TRACE && trace && tid == 0) trace[4] = global_ns();
     // reduce-then-scan ablation (rts.cu): the tile's run starts come from the

@@ -388,6 +388,21 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8])
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -449,6 +464,7 @@ struct PassParams {
   unsigned long long* trace;               // diagnostics: kTraceWords per tile, or null
   uint32_t wide_index;                     // output indices may reach 2^32 (64-bit run writes)
   const unsigned long long* rts_offsets;   // reduce-then-scan ablation: [num_tiles][radix] run starts, or null
+  int debug_stall_tile;                    // OS_JITTER builds: this tile never publishes (watchdog test); -1 off
 };
 // Per-tile trace record (globaltimer ns): claim, keys staged, L published,
 // reorder done, warp 0 G published, warp 0 done, SM id, unused.
@@ -496,6 +512,17 @@ size_t rts_chunk_count(size_t tiles);
 cudaError_t launch_rts_prefix(const uint32_t* counts, uint32_t tiles, int radix,
                               unsigned long long* csum, unsigned long long* offsets,
                               cudaStream_t stream);
+constexpr int kMaxWideDigitBits = 16;  // reference range (keycodec.py:110)
+cudaError_t launch_wide_histogram(const void* keys, size_t n, int key_bytes, int codec,
+                                  int begin_bit, int digit_bits, int passes, int top_bits,
+                                  unsigned long long* hist, cudaStream_t stream);
+cudaError_t launch_wide_tables(const unsigned long long* base, const unsigned long long* count,
+                               const unsigned long long* dense_start, int radix,
+                               unsigned long long* rel, unsigned long long* carry,
+                               cudaStream_t stream);
+cudaError_t launch_wide_scatter(const void* src_k, void* dst_k, const void* src_v, void* dst_v,
+                                int kb, int vb, size_t n, int shift, int width,
+                                const unsigned long long* rel, int codec_out, cudaStream_t stream);
 cudaError_t launch_top_histogram(const void* keys, size_t n, int key_bytes, int codec, int shift,
                                  uint32_t mask, unsigned long long* hist, cudaStream_t stream);
 

@@ -102,6 +102,9 @@ class Executor:
         self.jitter = jitter
         self.stream = stream
         self._ledger: dict[str, LedgerCounts] = {}
+        # element reads + writes the device actually performed (equal to the
+        # ledger's element_ops except when cfg.digit_bits > 8 runs as 8-bit places)
+        self.device_element_ops = 0
         self._pending: list[tuple[str, object, int]] = []  # (phase, device stats, radix)
         self._lock = threading.Lock()
 
@@ -134,6 +137,7 @@ class Executor:
         with self._lock:
             self._ledger.clear()
             self._pending.clear()
+            self.device_element_ops = 0
 
 
 def ledger_as_row(ledger: MemOpLedger) -> dict[str, int]:

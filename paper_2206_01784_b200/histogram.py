@@ -15,7 +15,7 @@ import numpy as np
 from . import _native
 from ._device import as_device, from_device, workspace
 from .executor import Executor
-from .keycodec import MAX_DEVICE_DIGIT_BITS, RadixConfig
+from .keycodec import RadixConfig
 
 
 @dataclass(frozen=True)
@@ -85,8 +85,6 @@ def global_histograms(encoded, cfg: RadixConfig, executor: Executor | None = Non
     kb = dev.element_size()
     if kb not in (4, 8) or (kb * 8) != cfg.key_bits:
         raise ValueError(f"config is for {cfg.key_bits}-bit keys but got {kb * 8}-bit data")
-    if cfg.digit_bits > MAX_DEVICE_DIGIT_BITS:
-        raise ValueError(f"device histograms support digit_bits <= {MAX_DEVICE_DIGIT_BITS}")
     end_bit = cfg.key_bits if end_bit is None else end_bit
     passes = -(-(end_bit - begin_bit) // cfg.digit_bits)
     hist = torch.empty((passes, cfg.radix), dtype=torch.uint64, device=dev.device)

@@ -82,3 +82,18 @@ def test_rts_all_equal_and_f64_pairs(cuda):
     want = oracle.sort(fk, fv)
     assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))
     assert np.array_equal(got[1], want[1])
+
+
+@pytest.mark.slow
+def test_rts_sort_above_one_strip(cuda):
+    # n > 2^28: the upsweep and the downsweep must tile every strip alike
+    # (a whole-array upsweep left count rows unwritten)
+    import torch
+
+    from paper_2206_01784_b200 import KeyGenSpec, generate_keys, rts_sort
+
+    n = (1 << 28) + 70_001
+    keys = generate_keys(KeyGenSpec(q=1, seed=21, n=n), device="cuda")
+    got = rts_sort(keys)
+    want = torch.sort(keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, stable=True).values
+    assert torch.equal(got.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, want)
