@@ -122,17 +122,39 @@ class ClockSampler:
         }
 
 
-def cpu_port_sort(n: int, threads: int, seed: int = 0) -> tuple[float, dict]:
+_CPU_KEYS: dict = {}
+
+
+def cpu_port_sort(n: int, threads: int, seed: int = 0, tile: int = 4096) -> tuple[float, dict]:
     """Time the oracle's C port of the reference onesweep_sort on the host."""
     from oracle import oracle
 
-    keys = oracle.keygen(n, 1, seed)
-    oracle.sort(keys[: 1 << 16], tile=4096, threads=threads)  # warm the pages / threads
+    if (n, seed) not in _CPU_KEYS:
+        _CPU_KEYS.clear()
+        _CPU_KEYS[(n, seed)] = oracle.keygen(n, 1, seed)
+    keys = _CPU_KEYS[(n, seed)]
+    oracle.sort(keys[: 1 << 16], tile=tile, threads=threads)  # warm the pages / threads
     t0 = time.perf_counter()
-    out = oracle.sort(keys, tile=4096, threads=threads)
+    out = oracle.sort(keys, tile=tile, threads=threads)
     dt = time.perf_counter() - t0
     assert out.size == n
     return dt, {"n": n}
+
+
+def cpu_numpy_oracle(n: int, seed: int = 0) -> float:
+    """Time the reference's oracle_stable_sort (baseline.py:27-34: stable
+    numpy argsort of the keys + gather) on the host, one thread."""
+    import numpy as np
+
+    from oracle import oracle
+
+    keys = oracle.keygen(n, 1, seed)
+    t0 = time.perf_counter()
+    order = np.argsort(keys, kind="stable")
+    out = keys[order]
+    dt = time.perf_counter() - t0
+    assert out.size == n
+    return dt
 
 
 def run_reference(args) -> None:
@@ -140,7 +162,7 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n = args.cpu_sample
+    n = args.n  # the GPU arm's exact workload (C2: 2^28 keys), one full sort per step
     for _ in range(args.warmup):
         cpu_port_sort(n, threads)
     times = [cpu_port_sort(n, threads)[0] for _ in range(args.steps)]
@@ -162,8 +184,10 @@ def run_reference(args) -> None:
         "vs_baseline": value / PAPER_A100_GKEYS,
         "dtype": "u32",
         "data": "synthetic (reference keygen, q=1, seed 0)",
-        "config": {"workload": "C2 sample: uniform u32 keys-only, 8-bit digits, CPU port of the "
-                               "reference onesweep_sort (oracle/onesweep_oracle.c)", "n": n},
+        "config": {"workload": "C2: 256M uniform u32 keys-only, 8-bit digits, 1 histogram + 4 binning "
+                               "passes -- CPU port of the reference onesweep_sort "
+                               "(oracle/onesweep_oracle.c), reference default cfg (tile 4096)",
+                   "n": n, "same_config": n == N_PER_GPU},
         "cpu_baseline": {"value": value, "unit": "GKey/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GKey/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -180,10 +204,16 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank; --backend gloo lets several ranks share a device
+    # (tests/test_gpu_bench_multi.py runs the N>1 path on one B200 that way)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
 
     from paper_2206_01784_b200 import DeviceSorter, KeyGenSpec, generate_keys, _native, onesweep_sort
 
@@ -232,26 +262,30 @@ def run_ours(args) -> None:
     for _ in range(args.warmup):
         step()
     barrier()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    # one event per step boundary: per-step device times (median reported,
+    # BASELINE.md section 4); nothing is recorded between a step's kernels
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clocks:
         barrier()
-        t_start.record(stream)
+        marks[0].record(stream)
         for i in range(args.steps):
-            step()  # plain sorts: no events between the kernels
-        t_end.record(stream)
+            step()
+            marks[i + 1].record(stream)
         barrier()
-    ms_local = t_start.elapsed_time(t_end) / args.steps
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    ms_local = statistics.median(step_ms)
     if world == 1:
         # per-kernel split from a separate instrumented run (events between
         # the kernels), outside the timed region
         for i in range(args.steps):
             step(i)
         torch.cuda.synchronize()
-    ms = torch.tensor([ms_local], device=dev)
+    cdev = dev if world == 1 or dist.get_backend() == "nccl" else "cpu"  # collectives' device
+    ms = torch.tensor([ms_local, statistics.mean(step_ms)], device=cdev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_per_step = float(ms.item())
+    ms_per_step = float(ms[0].item())
+    ms_mean = float(ms[1].item())
     total_keys = n * world
     value = total_keys / (ms_per_step * 1e-3) / 1e9
 
@@ -266,6 +300,8 @@ def run_ours(args) -> None:
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
+        "ms_per_step_mean": ms_mean,
+        "timing": f"median of {args.steps} per-step CUDA-event times (max over ranks)",
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": value / PAPER_A100_GKEYS,
@@ -315,9 +351,8 @@ def run_ours(args) -> None:
             "binning_pass_us": pass_us,
             "share_binning": sum(pass_us) / (ms_per_step * 1e3),
         }
-        # correctness spot check of the timed output (cheap, outside timing)
-        o = out[: 1 << 20].cpu().numpy()
-        line["output_sorted_prefix"] = bool((o[1:] >= o[:-1]).all())
+        # the whole timed output against an independent sort (outside timing)
+        line["output_verified"] = _verify_full(keys, out)
 
         # e2e: public API, host (pinned) buffers in, host array out, per step
         if args.e2e_steps > 0:
@@ -365,15 +400,23 @@ def run_ours(args) -> None:
             del pipe, outs_h, keys_h, keys_np
         if args.cpu_baseline and rank == 0:
             threads = os.cpu_count() or 1
-            dt, _ = cpu_port_sort(args.cpu_sample, threads)
+            m = args.cpu_sample
+            dt, _ = cpu_port_sort(m, threads)
+            dt_tuned, _ = cpu_port_sort(m, threads, tile=1 << 20)
+            dt_np = cpu_numpy_oracle(1 << 26)
             line["cpu_baseline"] = {
-                "value": args.cpu_sample / dt / 1e9, "unit": "GKey/s", "cores": threads,
+                "value": m / dt / 1e9, "unit": "GKey/s", "cores": threads,
                 "kind": "port",
-                "sample": f"2^{args.cpu_sample.bit_length() - 1} keys of the C2 distribution "
-                          "(keygen q=1 seed 0), C port of reference onesweep_sort, tile 4096, one run",
+                "sample": f"2^{m.bit_length() - 1} keys of the C2 distribution (keygen q=1 seed 0), "
+                          f"C port of the reference onesweep_sort, reference default tile 4096, "
+                          f"{threads} threads, one run",
+                "tuned_tile_2e20": {"value": m / dt_tuned / 1e9, "unit": "GKey/s", "cores": threads},
+                "oracle_stable_sort": {"value": (1 << 26) / dt_np / 1e9, "unit": "GKey/s", "cores": 1,
+                                       "sample": "2^26 keys, numpy argsort(kind='stable') + gather "
+                                                 "(baseline.py:27-34)"},
             }
     else:
-        line["e2e"] = sorter.e2e_line(keys, args.e2e_steps) if hasattr(sorter, "e2e_line") else None
+        _sharded_extras(line, args, sorter, keys, n, world, rank, cdev, peaks)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -382,16 +425,109 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def _verify_full(keys, out) -> bool:
+    """Every element of the timed output equals torch's stable sort of the
+    input (u32 compared as widened int64; a check only, outside timing)."""
+    import torch
+
+    a = keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    want = torch.sort(a, stable=True).values
+    del a
+    got = out.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    ok = bool(torch.equal(got, want))
+    del got, want
+    torch.cuda.empty_cache()
+    return ok
+
+
+def _sharded_extras(line, args, sorter, keys, n, world, rank, dev, peaks) -> None:
+    """N > 1: per-phase split, roofline of the local sort, end-to-end through
+    host buffers, and a global order check (all max over ranks).  `dev` is
+    where the small collectives run (the GPU for NCCL, the host for gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    kb = 4
+    # per-phase split from a separate instrumented run
+    reps = max(3, min(args.steps, 10))
+    acc: dict[str, list[float]] = {}
+    recv_n = 0
+    for _ in range(reps):
+        t: list = []
+        res = sorter(keys, timings=t)
+        recv_n = res.numel()
+        torch.cuda.synchronize()
+        for (a, ea), (b, eb) in zip(t, t[1:]):
+            acc.setdefault(b, []).append(ea.elapsed_time(eb))
+    names = ["split", "exchange", "local"]
+    ph = torch.tensor([statistics.median(acc[k]) for k in names], device=dev)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    line["phases_ms"] = {k: float(v) for k, v in zip(names, ph.tolist())}
+    local_ms = line["phases_ms"]["local"]
+    local_bytes = (1 + 2 * sorter.local_passes) * recv_n * kb
+    achieved = local_bytes / (local_ms * 1e-3) / 1e9
+    line["roofline"] = {
+        "kernel": "local Onesweep on each rank (1 histogram + 4 binning passes over the received keys)",
+        "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "peak_source": peaks["source"],
+        "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+        "algorithmic_bytes_per_launch": local_bytes, "launch_us": local_ms * 1e3,
+    }
+    # global order: each slice sorted, slices ordered across ranks, all keys kept
+    out = sorter(keys)
+    torch.cuda.synchronize()
+    o = out.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    local_ok = bool((o[1:] >= o[:-1]).all()) if o.numel() > 1 else True
+    ends = torch.tensor([o[0].item() if o.numel() else -1, o[-1].item() if o.numel() else -1,
+                         o.numel(), int(local_ok)], dtype=torch.int64, device=dev)
+    allends = [torch.empty_like(ends) for _ in range(world)]
+    dist.all_gather(allends, ends)
+    e = torch.stack(allends).cpu().tolist()
+    order_ok = all(e[r][1] <= e[r + 1][0] for r in range(world - 1) if e[r][2] and e[r + 1][2])
+    line["output_verified"] = bool(all(x[3] for x in e) and order_ok and sum(x[2] for x in e) == n * world)
+    del out, o
+    # end to end: host shard (pinned) -> device -> sharded sort -> host slice
+    if args.e2e_steps > 0:
+        keys_h = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+        keys_h.copy_(keys)
+        times, d2h = [], 0
+        for i in range(args.e2e_steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            kd = keys_h.to(keys.device, non_blocking=True)
+            res = sorter(kd)
+            res_h = torch.empty(res.numel(), dtype=torch.uint32, pin_memory=True)
+            res_h.copy_(res, non_blocking=True)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            if i:
+                times.append(t1 - t0)
+                d2h = res.numel() * kb
+            del kd, res, res_h
+        tt = torch.tensor([statistics.median(times), float(d2h)], device=dev, dtype=torch.float64)
+        tmax = tt.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        line["e2e"] = {"value": n * world / float(tmax[0]) / 1e9, "unit": "GKey/s",
+                       "h2d_bytes_per_step": n * world * kb, "d2h_bytes_per_step": int(tt[1]),
+                       "ms_per_step": float(tmax[0]) * 1e3, "steps": args.e2e_steps,
+                       "api": "paper_2206_01784_b200.distributed.ShardedSorter on each rank: pinned host "
+                              "shard in, sorted slice out (wall time, max over ranks)"}
+    else:
+        line["e2e"] = None
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--n-per-gpu", dest="n", type=int, default=N_PER_GPU)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--cpu-sample", type=int, default=N_PER_GPU)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--backend", default="nccl", help="process group backend for N > 1")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("timing rules need >= 3 warm-up steps")

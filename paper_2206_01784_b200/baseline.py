@@ -9,8 +9,13 @@ that table (baseline.py:76-84) and a downsweep scatter (baseline.py:87-118)
 -- where Onesweep's chained scan needs 2n.  On the device the downsweep is the
 Onesweep binning kernel with its look-back replaced by a read of the prefix
 table (os_rts_sort), so timing the two sorts isolates exactly what the single
-pass saves.  The reference's argsort ground truth (`oracle_stable_sort`) is
-test infrastructure and is not part of this package.
+pass saves.
+
+`oracle_stable_sort` is the reference's comparator API (baseline.py:27-34:
+stable argsort of the encoded keys + gather), kept for drop-in callers such as
+the CLI's `verify`.  It is deliberately *not* Onesweep: an independent order
+from torch's stable device sort of the encoded keys, so checking a Onesweep
+result against it is a real check.
 """
 
 from __future__ import annotations
@@ -92,11 +97,41 @@ def rts_sort(keys, values=None, cfg=None, executor: Executor | None = None):
     sorter = DeviceRtsSorter(n, dk.dtype, vb, device=dk.device)
     launch_on(executor.stream, (dk, ok, dv, ov, sorter.ws),
               lambda s: sorter(dk, ok, dv, ov, stream=s))
-    for _ in range(sorter.passes):  # baseline.py:70,116-117
+    # the configured plan's algorithmic traffic, 3n per place (baseline.py:70,
+    # 116-117); the device always runs 8-bit places (same output)
+    for _ in range(cfg.passes):
         executor.ledger_record("upsweep", "element_reads", n)
         executor.ledger_record("downsweep", "element_reads", n)
         executor.ledger_record("downsweep", "element_writes", n)
+    executor.device_element_ops += 3 * sorter.passes * n
     sk = from_device(ok, to_numpy)
     if values is None:
         return sk
     return sk, from_device(ov, to_numpy and not is_tensor(values))
+
+
+def oracle_stable_sort(keys, values=None):
+    """Stable ascending sort by encoded key order (baseline.py:27-34), by an
+    independent path: torch.sort(stable=True) of the encoded keys widened to
+    int64 in the same order, then a gather.  Same container type out as in."""
+    import torch
+
+    from .keycodec import encode_array
+
+    to_numpy = not is_tensor(keys)
+    if to_numpy:
+        keys = np.asarray(keys)
+    spec_for_dtype(keys.dtype)  # KeyError for unsupported dtypes
+    dk, _ = as_device(keys)
+    enc = encode_array(dk)
+    if enc.element_size() == 4:
+        order_key = enc.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    else:  # unsigned 64-bit order as signed: flip the top bit
+        order_key = enc.view(torch.int64) ^ (-(1 << 63))
+    order = torch.sort(order_key, stable=True).indices
+    sk = from_device(dk[order], to_numpy)
+    if values is None:
+        return sk
+    vnp = not is_tensor(values)
+    dv, _ = as_device(np.asarray(values) if vnp else values)
+    return sk, from_device(dv[order], vnp)

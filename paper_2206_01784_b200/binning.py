@@ -87,6 +87,70 @@ class SortBuffers:
         self.live_in_a = not self.live_in_a
 
 
+@dataclass(frozen=True)
+class TileRanking:
+    """Per-tile digit counts plus a stable tile-relative rank per element
+    (binning.py:41-46)."""
+
+    digit_counts: np.ndarray  # int64, length radix
+    ranks: np.ndarray  # int64, length tile
+
+
+def _device_rank(digits, digit_bits: int) -> TileRanking:
+    """Stable rank of every digit among equal digits, computed by the device
+    binning kernel: a stable partition of (digit, index) pairs, inverted.  The
+    kernel ranks by the same ballot multisplit as the reference's
+    rank_tile_kernel (_kernels.py:31-82)."""
+    import torch
+
+    d = np.asarray(digits, dtype=np.int64)
+    radix = 1 << digit_bits
+    if d.size == 0:
+        return TileRanking(np.zeros(radix, dtype=np.int64), np.zeros(0, dtype=np.int64))
+    if d.min() < 0 or d.max() >= radix:
+        raise ValueError(f"digits must lie in [0, {radix})")
+    cfg = radix_plan(32, digit_bits)
+    keys = d.astype(np.uint32)
+    from .histogram import global_bin_offsets, global_histograms
+
+    hist = global_histograms(keys, cfg)
+    base = global_bin_offsets(hist).offsets[0]
+    idx = np.arange(d.size, dtype=np.uint32)
+    dst = np.zeros_like(keys)
+    dvals = np.zeros_like(idx)
+    partition_pass(keys, dst, 0, base, cfg, None, idx, dvals)
+    slot = torch.empty(d.size, dtype=torch.int64, device="cuda")
+    slot[torch.from_numpy(dvals.astype(np.int64)).cuda()] = torch.arange(d.size, device="cuda")
+    dd = torch.from_numpy(d).cuda()
+    b = torch.from_numpy(base.astype(np.int64)).cuda()
+    ranks = (slot - b[dd]).cpu().numpy()
+    return TileRanking(hist.counts[0].astype(np.int64), ranks)
+
+
+def wlms_rank(digits, digit_bits: int):
+    """Rank one lane group of at most 32 digits (binning.py:50-68).  Returns
+    (counts[2^digit_bits], stable ranks); ValueError for more than 32."""
+    d = np.asarray(digits, dtype=np.int64)
+    if d.size > LANE_GROUP:
+        raise ValueError(f"lane group holds at most {LANE_GROUP} values")
+    r = _device_rank(d, digit_bits)
+    return r.digit_counts, r.ranks
+
+
+def rank_tile(digits, cfg: RadixConfig) -> TileRanking:
+    """Stable tile-wide ranking (binning.py:71-76), on the device."""
+    return _device_rank(digits, cfg.digit_bits)
+
+
+def short_circuit_check(ranking: TileRanking) -> int | None:
+    """The single digit covering the whole tile, or None (binning.py:79-85)."""
+    n = ranking.ranks.size
+    if n == 0:
+        return None
+    top = int(np.argmax(ranking.digit_counts))
+    return top if int(ranking.digit_counts[top]) == n else None
+
+
 def _val_bytes(values) -> int:
     if values is None:
         return 0

@@ -118,6 +118,11 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 // OS_SPIN_LIMIT times traps (the launch fails with cudaErrorLaunchFailure /
 // illegal instruction) instead of hanging the GPU.  A healthy pass waits a
 // few microseconds; 2^26 re-polls is over a minute of L2 round trips.
+// Back-off (ns) before re-polling an unpublished predecessor word: fewer
+// issue slots burnt by spinning digit threads.
+#ifndef OS_LB_BACKOFF
+#define OS_LB_BACKOFF 0
+#endif
 #ifndef OS_SPIN_LIMIT
 #define OS_SPIN_LIMIT (1u << 26)
 #endif
@@ -485,11 +490,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
-    if (P.rts_offsets == nullptr)  // (reduce-then-scan passes have no look-back)
+    if (P.rts_offsets == nullptr) {  // (reduce-then-scan passes have no look-back)
       if (OS_JITTER) jitter_sleep(tile, tid, 1);
       if (!OS_JITTER || int(tile) != P.debug_stall_tile)
-      status_st(P.status + size_t(tile) * radix + tid,
-                (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+        status_st(P.status + size_t(tile) * radix + tid,
+                  (tile == 0 ? kFlagGlobal : kFlagLocal) | count);
+    }
     if (count == valid) s_fast = tid;
   }
   if (OS_TRACE && trace && tid == 0) trace[2] = global_ns();
@@ -615,6 +621,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           const uint32_t st = w[k] >> kStatusShift;
           if (st == 0u) {  // predecessor in flight: re-poll from here
             ++waits;
+            if (OS_LB_BACKOFF > 0) __nanosleep(OS_LB_BACKOFF);
             if (++spins > OS_SPIN_LIMIT) {
               printf("onesweep: look-back stalled (tile %u digit %d waits on tile %d)\n", tile, tid,
                      j - k);

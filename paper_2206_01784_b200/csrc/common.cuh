@@ -336,17 +336,33 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// OS_MBAR_HINT > 0: try_wait carries a suspend-time hint (ns), so a waiting
+// thread sleeps until the phase completes (or the hint expires) instead of
+// re-issuing the try_wait loop, leaving issue slots to the other blocks.
+#ifndef OS_MBAR_HINT
+#define OS_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t addr = smem_u32(bar);
   while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
+    if (OS_MBAR_HINT > 0) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(addr), "r"(parity), "r"(uint32_t(OS_MBAR_HINT))
+          : "memory");
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(addr), "r"(parity)
+          : "memory");
+    }
   }
 }
 // One bulk (non-tensor) TMA copy; bytes % 16 == 0, both addresses 16B aligned.

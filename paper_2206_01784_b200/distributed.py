@@ -247,7 +247,7 @@ def _p2p_usable(keys, values, group) -> bool:
 
 
 def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = SPLIT_DIGIT_BITS,
-                 return_plan: bool = False, exchange: str = "auto"):
+                 return_plan: bool = False, exchange: str = "auto", timings: list | None = None):
     """Stable sort of the global array whose rank-order concatenation is
     `keys` over all ranks of `group`.  Returns this rank's contiguous slice
     of the sorted output (and values).
@@ -255,7 +255,12 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     exchange: "p2p" (fused partition + peer stores), "all_to_all"
     (partition + all_to_all_single; staged through the host for non-NCCL
     groups), or "auto" (p2p when the group is NCCL and symmetric memory is
-    available, else all-to-all)."""
+    available, else all-to-all).
+
+    timings: if a list is given, (phase, CUDA event) pairs are appended at
+    the phase boundaries on the current stream -- "start", "split" (top
+    histogram + all_gather + plan), "exchange" (partition + exchange),
+    "local" (local Onesweep) -- for bench.py's per-phase split."""
     global _P2P_BROKEN
     import torch
     import torch.distributed as dist
@@ -267,6 +272,14 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     if values is not None and values.shape != keys.shape:
         raise ValueError("values must have the same length as keys")
 
+    def mark(name):
+        if timings is not None and keys.is_cuda:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            timings.append((name, ev))
+
+    mark("start")
+
     hist = ops.top_histogram(keys, spec, digit_bits)
     backend = dist.get_backend(group)
     h64 = hist.view(torch.int64)
@@ -277,6 +290,7 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     table = torch.stack(gathered).cpu().numpy().view(np.uint64)
     bin_lo = plan_split(table, world)
     send, recv = exchange_counts(table, bin_lo, rank)
+    mark("split")
 
     rb = None
     want_p2p = exchange == "p2p" or (exchange == "auto" and _p2p_usable(keys, values, group))
@@ -319,7 +333,9 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
         part_k, part_v = ops.partition(keys, values, spec, digit_bits, bin_lo, send)
         recv_k = _all_to_all(part_k, send, recv, group)
         recv_v = _all_to_all(part_v, send, recv, group) if values is not None else None
+    mark("exchange")
     out_k, out_v = ops.local_sort(recv_k, recv_v)
+    mark("local")
     result = out_k if values is None else (out_k, out_v)
     if return_plan:
         return result, {"bin_lo": bin_lo, "send": send, "recv": recv, "exchange": exchange}
@@ -439,5 +455,5 @@ class ShardedSorter:
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
         return "p2p" if int(flag.item()) == 1 else "all_to_all"
 
-    def __call__(self, keys, values=None):
-        return sharded_sort(keys, values, self.group, exchange=self.exchange)
+    def __call__(self, keys, values=None, timings=None):
+        return sharded_sort(keys, values, self.group, exchange=self.exchange, timings=timings)

@@ -90,6 +90,27 @@ class Jitter:
         return None
 
 
+class TileTicket:
+    """Shared monotone counter issuing each tile index in [0, tiles) exactly
+    once (executor.py:88-105).  The device kernels take their tile ids from an
+    atomicAdd on a ticket word (csrc/binning.cu); this host twin keeps the
+    reference's API for callers that schedule their own work."""
+
+    def __init__(self, tiles: int):
+        self._tiles = tiles
+        self._next = 0
+        self._lock = threading.Lock()
+
+    def next_tile(self) -> int | None:
+        """Next tile index, or None once all tiles have been issued."""
+        with self._lock:
+            if self._next >= self._tiles:
+                return None
+            tile = self._next
+            self._next += 1
+            return tile
+
+
 class Executor:
     """Ledger owner for device sorts (executor.py:124-156)."""
 
@@ -147,4 +168,4 @@ def ledger_as_row(ledger: MemOpLedger) -> dict[str, int]:
     return row
 
 
-__all__ = ["Executor", "Jitter", "LedgerCounts", "MemOpLedger", "ledger_as_row"]
+__all__ = ["Executor", "Jitter", "LedgerCounts", "MemOpLedger", "TileTicket", "ledger_as_row"]

@@ -68,3 +68,21 @@ def expected_entropy(q: int) -> float:
     if q < 1:
         raise ValueError(f"q must be >= 1, got {q}")
     return binary_entropy(2.0 ** -q)
+
+
+def empirical_bit_entropy(keys) -> float:
+    """Mean over bit positions of H(fraction of ones at that bit)
+    (keygen.py:94-105).  Counted on the device: one popcount reduction per bit
+    position over the keys (numpy input is uploaded once)."""
+    import torch
+
+    from ._device import as_device
+
+    dev, _ = as_device(keys)
+    n = dev.numel()
+    if n == 0:
+        raise ValueError("empirical_bit_entropy requires at least one key")
+    width = dev.element_size() * 8
+    w = dev.view(torch.int32 if width == 32 else torch.int64)
+    ones = torch.stack([((w >> b) & 1).sum(dtype=torch.int64) for b in range(width)]).tolist()
+    return sum(binary_entropy(c / n) for c in ones) / width

@@ -167,13 +167,24 @@ def test_executor_ledger():
 
 
 def test_product_never_imports_oracle():
+    # the product package never imports, loads or links the test oracle
+    # (oracle/, liboracle.so); "oracle" as the reference CLI's algo name and
+    # the comparator API oracle_stable_sort are not the oracle package
     pkg = os.path.join(ROOT, "paper_2206_01784_b200")
+    bad = re.compile(r"(^|\n)\s*(from\s+oracle\b|import\s+oracle\b)|liboracle|or_sort|oracle/")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
             if f.endswith((".py", ".cu", ".cuh")):
-                text = open(os.path.join(dirpath, f)).read()
-                assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle_stable_sort", "") \
-                    or f == "__init__.py", f
+                text = re.sub(r"#.*|//.*", "", open(os.path.join(dirpath, f)).read())
+                assert not bad.search(text), f
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r); import paper_2206_01784_b200, paper_2206_01784_b200.cli, "
+            "paper_2206_01784_b200.distributed; print(any(m == 'oracle' or m.startswith('oracle.') "
+            "for m in sys.modules))" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.stdout.strip() == "False", out.stdout + out.stderr
 
 
 def test_entropy_table():

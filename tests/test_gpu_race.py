@@ -55,10 +55,11 @@ for n, dt, d, tile, strip, vals in [
     v = np.arange(n, dtype=np.uint32) if vals else None
     got = onesweep_sort(keys, v, cfg if tile else None)
     want = oracle.sort(keys, v, digit_bits=d)
+    u = np.uint64 if bits == 64 else np.uint32  # bit patterns: NaN keys compare equal
     if vals:
-        assert np.array_equal(got[0].view(want[0].dtype), want[0]) and np.array_equal(got[1], want[1]), (n, dt)
+        assert np.array_equal(got[0].view(u), want[0].view(u)) and np.array_equal(got[1], want[1]), (n, dt)
     else:
-        assert np.array_equal(got.view(want.dtype), want), (n, dt)
+        assert np.array_equal(got.view(u), want.view(u)), (n, dt)
     cases += 1
 # a pass's final status words under jitter equal the sequential CounterMatrix
 src = rng.integers(0, 2**32, size=40_000, dtype=np.uint32)
