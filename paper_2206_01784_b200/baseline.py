@@ -129,9 +129,17 @@ def oracle_stable_sort(keys, values=None):
     else:  # unsigned 64-bit order as signed: flip the top bit
         order_key = enc.view(torch.int64) ^ (-(1 << 63))
     order = torch.sort(order_key, stable=True).indices
-    sk = from_device(dk[order], to_numpy)
+    sk = from_device(_take(dk, order), to_numpy)
     if values is None:
         return sk
     vnp = not is_tensor(values)
     dv, _ = as_device(np.asarray(values) if vnp else values)
-    return sk, from_device(dv[order], vnp)
+    return sk, from_device(_take(dv, order), vnp)
+
+
+def _take(t, order):
+    """t[order] by bit pattern (CUDA has no gather for the unsigned dtypes)."""
+    import torch
+
+    signed = {1: torch.int8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[t.element_size()]
+    return t.view(signed)[order].view(t.dtype)

@@ -140,11 +140,20 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_RANK_STASH
 #define OS_RANK_STASH 0  // 1: keys-only passes park the packed ranks in TMEM too
 #endif
+// 1: the ranking loop takes each digit's running count with one shared-memory
+// atomic by the digit's highest lane (old value broadcast with a shuffle)
+// instead of a counter load by every lane plus a store by the leader; the
+// per-warp counters are then 32-bit.
+#ifndef OS_RANK_ATOMIC
+#define OS_RANK_ATOMIC 0
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
 
 constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
+
+constexpr int kCounterBytes = OS_RANK_ATOMIC ? 4 : 2;  // per-warp digit counter width
 
 template <int THREADS, int ITEMS, int KB, int VB>
 struct BinningSmem {
@@ -153,7 +162,7 @@ struct BinningSmem {
   static constexpr size_t kKeys = size_t(kTile) * KB;
   static constexpr size_t kVals = (size_t(kTile) * VB + 15) / 16 * 16;
   // per-warp u16 digit counters, later the warp's slot offsets
-  static constexpr size_t kHist = (size_t(kWarps) * kMaxRadix * 2 + 15) / 16 * 16;
+  static constexpr size_t kHist = (size_t(kWarps) * kMaxRadix * kCounterBytes + 15) / 16 * 16;
   static constexpr size_t kPtr = kMaxRadix * 8;  // per-digit 64-bit output index (keys, values)
   static constexpr size_t kRel = kMaxRadix * 4;  // per-digit 32-bit output index
   static constexpr size_t kLocal = kMaxRadix * 4;  // tile-local digit starts
@@ -191,7 +200,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   VS* s_vals = reinterpret_cast<VS*>(smem_raw + Smem::kKeys);
-  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem_raw + Smem::kKeys + Smem::kVals);
+  using CT = typename std::conditional<kCounterBytes == 4, uint32_t, uint16_t>::type;
+  CT* s_whist = reinterpret_cast<CT*>(smem_raw + Smem::kKeys + Smem::kVals);
   unsigned long long* s_ptr = reinterpret_cast<unsigned long long*>(
       smem_raw + Smem::kKeys + Smem::kVals + Smem::kHist);
   uint32_t* s_rel = reinterpret_cast<uint32_t*>(s_ptr + kMaxRadix);
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // multiply-add operands for the index arithmetic (see fma_u32): written as
   // mad.lo, ptxas keeps these as IMADs on the FMA pipe (742 vs 808 us/pass,
   // profiles/round1_binning_notes.md)
-  constexpr uint32_t k_one = 1u, k_two = 2u, k_shl16 = 1u << 16;
+  constexpr uint32_t k_one = 1u, k_two = 2u, k_shl16 = 1u << 16, k_cw = uint32_t(kCounterBytes);
   // look-back status words (lookback.py:63-79), optionally kept in L2
   const uint64_t status_pol = OS_STATUS_KEEP ? l2_policy_evict_last() : 0ull;
   auto status_ld = [&](const uint32_t* a) -> uint32_t {
@@ -397,7 +407,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     const int w = RSTASH ? (i / 2) & 3 : i / 2;
     return (i & 1) ? (ranks[w] >> 16) : (ranks[w] & 0xffffu);
   };
-  const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * 2);
+  const uint32_t hbase = smem_u32(s_whist) + uint32_t(warp) * (kMaxRadix * kCounterBytes);
   auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint32_t lt = lanemask_lt();
@@ -429,13 +439,27 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         d = idx < valid ? digit(x) : uint32_t(radix - 1);
       uint32_t upto;
       bool leader;
-      match_rank8(d, le, ~le, &upto, &leader);
-      const uint32_t caddr = fma_u32(d, k_two, hbase);
-      const uint32_t rank = lds_u16(caddr) + __popc(upto) * KB;
-      put_rank(i, rank);
-      if (OS_SYNCWARP & 1) __syncwarp();
-      if (leader) sts_u16(caddr, rank);
-      if (OS_SYNCWARP & 2) __syncwarp();
+      if constexpr (OS_RANK_ATOMIC) {
+        // the highest lane of each digit adds the digit's count and gets the
+        // running count before this item; its peers take it by shuffle
+        uint32_t peers;
+        match_rank8_peers(d, le, &upto, &peers);
+        const uint32_t src = 31u - __clz(peers);
+        const uint32_t cnt = __popc(upto) * KB;
+        uint32_t old = 0;
+        if (src == uint32_t(lane)) old = atoms_add_u32(fma_u32(d, k_cw, hbase), cnt);
+        old = __shfl_sync(0xffffffffu, old, src);
+        put_rank(i, old + cnt);
+        if (OS_SYNCWARP & 2) __syncwarp();
+      } else {
+        match_rank8(d, le, ~le, &upto, &leader);
+        const uint32_t caddr = fma_u32(d, k_two, hbase);
+        const uint32_t rank = lds_u16(caddr) + __popc(upto) * KB;
+        put_rank(i, rank);
+        if (OS_SYNCWARP & 1) __syncwarp();
+        if (leader) sts_u16(caddr, rank);
+        if (OS_SYNCWARP & 2) __syncwarp();
+      }
     }
   };
   // A warp whose keys all carry one digit needs no multisplit: its inclusive
@@ -462,7 +486,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (uniform_warp) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) put_rank(i, uint32_t(i * 32 + lane + 1) * KB);
-        if (lane == 0) sts_u16(hbase + d0 * 2u, uint32_t(ITEMS * 32 * KB));
+        if (lane == 0) {
+          if constexpr (kCounterBytes == 4)
+            sts_u32(hbase + d0 * 4u, uint32_t(ITEMS * 32 * KB));
+          else
+            sts_u16(hbase + d0 * 2u, uint32_t(ITEMS * 32 * KB));
+        }
         if constexpr (STASH) {  // the keys still go to the stash
 #pragma unroll
           for (int i = 0; i < ITEMS; ++i) {
@@ -521,7 +550,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {  // counts re-read: registers are scarce here
       const uint32_t c = s_whist[w * kMaxRadix + tid];
-      s_whist[w * kMaxRadix + tid] = uint16_t(run);
+      s_whist[w * kMaxRadix + tid] = CT(run);
       run += c;
     }
   }
@@ -568,7 +597,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           key = keys[i];
         const uint32_t r = get_rank(i);  // (a warp-collective TMEM load under RSTASH)
         if (!FULL && warp_base + i * 32 + lane >= valid) continue;
-        const uint32_t off = lds_u16(fma_u32(digit(key), k_two, hbase));
+        uint32_t off;
+        if constexpr (kCounterBytes == 4)
+          off = lds_u32(fma_u32(digit(key), k_cw, hbase));
+        else
+          off = lds_u16(fma_u32(digit(key), k_two, hbase));
         const uint32_t addr = fma_u32(off, k_one, fma_u32(r, k_one, slot0));
         sts_val(addr, key);
         if (HAS_V) {

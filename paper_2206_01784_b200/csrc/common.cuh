@@ -149,6 +149,26 @@ __device__ __forceinline__ void match_rank8(uint32_t d, uint32_t sel, uint32_t g
   *leader = and3(c, v7, gt) == 0u;
 }
 
+// Same peer mask as match_rank8, returned whole: `peers` is every lane with
+// this lane's digit, `peers_sel` the ones in `sel`.
+__device__ __forceinline__ void match_rank8_peers(uint32_t d, uint32_t sel, uint32_t* peers_sel,
+                                                  uint32_t* peers) {
+  const uint32_t v0 = vote_bit(d, 1), v1 = vote_bit(d, 2), v2 = vote_bit(d, 4),
+                 v3 = vote_bit(d, 8), v4 = vote_bit(d, 16), v5 = vote_bit(d, 32),
+                 v6 = vote_bit(d, 64), v7 = vote_bit(d, 128);
+  const uint32_t c = and3(and3(v0, v1, v2), and3(v3, v4, v5), v6);
+  *peers_sel = and3(c, v7, sel);
+  *peers = c & v7;
+}
+
+// Shared-memory atomic add returning the old value (volatile: stays in
+// program order with the other volatile shared accesses).
+__device__ __forceinline__ uint32_t atoms_add_u32(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+  return old;
+}
+
 // Shared-memory accesses by 32-bit shared address.  Volatile, so ptxas keeps
 // them in program order relative to each other (the ranking counters are
 // read and rewritten by the same warp item after item), but without a memory

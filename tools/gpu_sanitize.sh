@@ -8,7 +8,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = "memcheck" ] && extra="--leak-check full"
   [ "$tool" = "racecheck" ] && extra="--racecheck-report all"
-  timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 50 python tools/sanitize_cases.py "$@" \
+  PYTORCH_NO_CUDA_MEMORY_CACHING=1 timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 50 python tools/sanitize_cases.py "$@" \
     > gpurun_out/sanitize_${tool}_$TAG.log 2>&1
   echo "$tool rc=$? $(grep -c 'case ok' gpurun_out/sanitize_${tool}_$TAG.log) cases ok; $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_${tool}_$TAG.log | tail -1)"
 done
