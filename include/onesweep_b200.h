@@ -204,6 +204,30 @@ int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* 
                 size_t n, int key_type, int val_bytes, void* workspace,
                 size_t workspace_bytes, void** events, int num_events, void* stream);
 
+/* ---- reduce-then-scan building blocks, one digit place each -------------
+ * os_rts_upsweep       replaces rts_upsweep      (baseline.py:55-73):
+ *   counts u32[tiles][2^digit_width] of keys (codec applied first) in tiles
+ *   of tile_keys (any size).
+ * os_rts_block_prefix  replaces rts_block_prefix (baseline.py:76-84):
+ *   digit-major exclusive prefix of that table -> u64[tiles][radix] absolute
+ *   run starts; workspace os_rts_prefix_workspace_bytes(tiles, radix).
+ * os_rts_downsweep     replaces rts_downsweep    (baseline.py:87-118):
+ *   stable scatter of each tile seeded by its offsets row (the binning kernel
+ *   without the look-back); tile_keys <= os_tile_capacity(key, val bytes),
+ *   equal to the upsweep's; workspace os_rts_downsweep_workspace_bytes().
+ * digit_width in [1, 8], n < 2^32. */
+int os_rts_upsweep(const void* keys, size_t n, int key_bytes, int codec, int shift, int digit_width,
+                   int tile_keys, unsigned int* counts, void* stream);
+size_t os_rts_prefix_workspace_bytes(size_t tiles, int radix);
+int os_rts_block_prefix(const unsigned int* counts, size_t tiles, int radix,
+                        unsigned long long* offsets, void* workspace, size_t workspace_bytes,
+                        void* stream);
+size_t os_rts_downsweep_workspace_bytes(void);
+int os_rts_downsweep(const void* src_keys, void* dst_keys, const void* src_vals, void* dst_vals,
+                     size_t n, int key_bytes, int val_bytes, int shift, int digit_width,
+                     const unsigned long long* offsets, int tile_keys, int codec_in,
+                     int codec_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fused partition + exchange over peer memory (NVLink): like
  * os_msd_partition, but dest_index is a device u64[parts] of element indices,
  * relative to keys_out / vals_out, where this rank's segment starts in each

@@ -59,6 +59,11 @@ SIGNATURES = {
     "os_msd_partition_p2p": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),
     "os_rts_sort_workspace_bytes": (_sz, [_sz, _i, _i]),
     "os_rts_sort": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp, _i, _vp]),
+    "os_rts_upsweep": (_i, [_vp, _sz, _i, _i, _i, _i, _i, _vp, _vp]),
+    "os_rts_prefix_workspace_bytes": (_sz, [_sz, _i]),
+    "os_rts_block_prefix": (_i, [_vp, _sz, _i, _vp, _vp, _sz, _vp]),
+    "os_rts_downsweep_workspace_bytes": (_sz, []),
+    "os_rts_downsweep": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _sz, _vp]),
 }
 
 

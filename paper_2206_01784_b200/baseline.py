@@ -20,12 +20,14 @@ result against it is a real check.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from . import _native
 from ._device import as_device, from_device, is_tensor, launch_on, workspace
 from .executor import Executor
-from .keycodec import radix_plan, spec_for_dtype
+from .keycodec import MAX_DEVICE_DIGIT_BITS, radix_plan, spec_for_dtype
 
 
 class DeviceRtsSorter:
@@ -108,6 +110,118 @@ def rts_sort(keys, values=None, cfg=None, executor: Executor | None = None):
     if values is None:
         return sk
     return sk, from_device(ov, to_numpy and not is_tensor(values))
+
+
+@dataclass(frozen=True)
+class BlockHistogramTable:
+    """(tiles, radix) per-tile digit counts of one digit place
+    (baseline.py:37-48)."""
+
+    counts: np.ndarray
+
+    @property
+    def tiles(self) -> int:
+        return self.counts.shape[0]
+
+    @property
+    def radix(self) -> int:
+        return self.counts.shape[1]
+
+
+def _rts_width(cfg) -> int:
+    if cfg.digit_bits > MAX_DEVICE_DIGIT_BITS:
+        raise ValueError(f"the device rts passes run digit widths <= {MAX_DEVICE_DIGIT_BITS}, "
+                         f"got {cfg.digit_bits}")
+    return cfg.digit_bits
+
+
+def rts_upsweep(encoded, place: int, cfg, executor: Executor | None = None) -> BlockHistogramTable:
+    """First data pass of the comparator (baseline.py:55-73): per-tile digit
+    counts of already-encoded keys, n element reads, on the device
+    (csrc/rts.cu rts_upsweep_kernel via os_rts_upsweep)."""
+    import torch
+
+    executor = executor or Executor()
+    width = _rts_width(cfg)
+    dk, _ = as_device(encoded)
+    n = dk.numel()
+    tiles = -(-n // cfg.tile_size)
+    counts = torch.zeros(max(tiles * cfg.radix, 1), dtype=torch.int32, device=dk.device)
+    L = _native.load()
+    launch_on(executor.stream, (dk, counts), lambda s: _native.check(
+        L.os_rts_upsweep(_native.ptr(dk), n, dk.element_size(), _native.CODEC_NONE,
+                         cfg.digit_shift(place), width, cfg.tile_size, _native.ptr(counts),
+                         _native.stream_handle(s)), "rts_upsweep"))
+    if n:
+        executor.ledger_record("upsweep", "element_reads", n)
+    table = counts[: tiles * cfg.radix].view(torch.uint32).cpu().numpy().astype(np.int64)
+    return BlockHistogramTable(table.reshape(tiles, cfg.radix))
+
+
+def rts_block_prefix(table: BlockHistogramTable) -> np.ndarray:
+    """Exclusive prefix over the digit-major linearisation of the table
+    (baseline.py:76-84): entry [tile, digit] is the absolute output start of
+    that tile's digit run.  Device scan (os_rts_block_prefix)."""
+    import torch
+
+    counts = np.asarray(table.counts)
+    tiles, radix = counts.shape
+    if tiles == 0:
+        return np.zeros((0, radix), dtype=np.int64)
+    if counts.min(initial=0) < 0 or counts.max(initial=0) >= 1 << 32:
+        raise ValueError("tile counts must fit in 32 bits")
+    dc, _ = as_device(np.ascontiguousarray(counts.astype(np.uint32)))
+    out = torch.empty(tiles * radix, dtype=torch.int64, device=dc.device)
+    L = _native.load()
+    ws = workspace(L.os_rts_prefix_workspace_bytes(tiles, radix), dc.device)
+    _native.check(L.os_rts_block_prefix(_native.ptr(dc), tiles, radix, _native.ptr(out), _native.ptr(ws),
+                                        ws.numel(), _native.stream_handle(None)), "rts_block_prefix")
+    return out.cpu().numpy().reshape(tiles, radix)
+
+
+def rts_downsweep(encoded, place: int, offsets, out, cfg, executor: Executor | None = None,
+                  values=None, out_values=None) -> None:
+    """Second data pass (baseline.py:87-118): stable scatter of every tile
+    seeded by its row of `offsets` (n reads + n writes).  The device kernel is
+    the Onesweep binning kernel with the look-back replaced by the table
+    (os_rts_downsweep).  Numpy outputs are updated in place."""
+    import torch
+
+    executor = executor or Executor()
+    width = _rts_width(cfg)
+    dk, _ = as_device(encoded)
+    n = dk.numel()
+    if n == 0:
+        return
+    kb = dk.element_size()
+    off = offsets if is_tensor(offsets) else np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    doff, _ = as_device(off)
+    if doff.numel() != (-(-n // cfg.tile_size)) * cfg.radix:
+        raise ValueError("offsets must have one row of radix run starts per tile")
+    ok, _ = as_device(out)
+    dv = ov = None
+    vb = 0
+    if values is not None:
+        dv, _ = as_device(values)
+        ov, _ = as_device(out_values)
+        vb = dv.element_size()
+    L = _native.load()
+    ws = workspace(L.os_rts_downsweep_workspace_bytes(), dk.device)
+    launch_on(executor.stream, (dk, doff, ok, dv, ov, ws), lambda s: _native.check(
+        L.os_rts_downsweep(_native.ptr(dk), _native.ptr(ok), _native.ptr(dv), _native.ptr(ov), n, kb, vb,
+                           cfg.digit_shift(place), width, _native.ptr(doff), cfg.tile_size,
+                           _native.CODEC_NONE, _native.CODEC_NONE, _native.ptr(ws), ws.numel(),
+                           _native.stream_handle(s)), "rts_downsweep"))
+    executor.ledger_record("downsweep", "element_reads", n)
+    executor.ledger_record("downsweep", "element_writes", n)
+    for dst, dev in ((out, ok), (out_values, ov)):
+        if dst is None:
+            continue
+        if is_tensor(dst):
+            if dst.data_ptr() != dev.data_ptr():
+                dst.copy_(dev)
+        else:
+            np.copyto(dst, from_device(dev, True).view(np.asarray(dst).dtype))
 
 
 def oracle_stable_sort(keys, values=None):

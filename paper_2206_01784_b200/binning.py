@@ -363,3 +363,49 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
         views.append(CounterMatrix(words[pos: pos + tiles * cfg.radix].reshape(tiles, cfg.radix)))
         pos += tiles * cfg.radix
     return result, views
+
+
+def process_tile(tile_index: int, keys_tile, out_keys, place: int, base_offsets, counters,
+                 cfg: RadixConfig, values_tile=None, out_values=None, carry_out=None,
+                 jitter=None):
+    """One tile of a pass driven from the host (binning.py:162-215): the
+    tile's exclusive prefix comes from the predecessors' words in `counters`
+    (a host lookback.CounterMatrix), the tile is partitioned on the device by
+    os_partition_pass into `out_keys` at base + exclusive + rank, and the
+    tile's L and G words are published.  Returns the tile's LedgerCounts.
+
+    The sort itself never calls this: on the device every tile runs the whole
+    pipeline inside the binning kernel.  It exists for callers that drive
+    single tiles, as the reference's own tests do."""
+    import torch
+
+    from .executor import LedgerCounts
+
+    if jitter is not None:
+        jitter.pause()
+    exclusive, reads = counters.lookback_exclusive_row(tile_index)
+    base = np.asarray(base_offsets, dtype=np.uint64).astype(np.int64) + exclusive
+    n = _numel(keys_tile)
+    ex = Executor()
+    if n:
+        # (a tile larger than the device tile runs as several device tiles
+        # chained by the kernel's own look-back: same placement)
+        carry = partition_pass(keys_tile, out_keys, place, base.astype(np.uint64), cfg, ex,
+                               values_tile, out_values)
+        off = carry.offsets
+        total = off.to(torch.int64).cpu().numpy() if is_tensor(off) else off.astype(np.int64)
+        counts = total - base
+    else:
+        counts = np.zeros(cfg.radix, dtype=np.int64)
+    counters.publish_local_row(tile_index, counts)
+    if jitter is not None:
+        jitter.pause()
+    inclusive = exclusive + counts
+    counters.publish_inclusive_row(tile_index, inclusive)
+    counter_ops = 2 * cfg.radix + reads
+    if carry_out is not None:
+        carry_out[:] = np.asarray(base_offsets, dtype=np.uint64) + inclusive.astype(np.uint64)
+        counter_ops += cfg.radix
+    fast = int(n > 0 and counts.max() == n)
+    return LedgerCounts(element_reads=n, element_writes=n, counter_ops=counter_ops,
+                        fast_path_tiles=fast)

@@ -960,4 +960,99 @@ int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* 
   return OS_OK;
 }
 
+// ---- reduce-then-scan building blocks (baseline.py:55-118) ------------------
+// The reference's rts_upsweep / rts_block_prefix / rts_downsweep as separate
+// calls over one digit place, for callers that drive the comparator pass by
+// pass (the reference's own tests do).  One strip, n < 2^32, widths <= 8.
+int os_rts_upsweep(const void* keys, size_t n, int key_bytes, int codec, int shift, int digit_width,
+                   int tile_keys, unsigned int* counts, void* stream) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
+  if (digit_width < 1 || digit_width > kMaxDigitBits)
+    return fail(OS_ERR_ARG, "rts digit width must be in [1, %d]", kMaxDigitBits);
+  if (shift < 0 || shift >= key_bytes * 8) return fail(OS_ERR_ARG, "shift out of range");
+  if (codec < 0 || codec > 3) return fail(OS_ERR_ARG, "bad codec");
+  if (tile_keys <= 0) return fail(OS_ERR_ARG, "tile_keys must be > 0");
+  if (n >= (size_t(1) << 32)) return fail(OS_ERR_ARG, "rts passes support n < 2^32");
+  if (n == 0) return OS_OK;
+  OS_CUDA(launch_rts_upsweep(keys, n, key_bytes, uint32_t(tile_keys), shift,
+                             (1u << digit_width) - 1u, codec, counts,
+                             static_cast<cudaStream_t>(stream)),
+          "rts upsweep");
+  return OS_OK;
+}
+
+size_t os_rts_prefix_workspace_bytes(size_t tiles, int radix) {
+  if (radix < 1 || radix > kMaxRadix) return 0;
+  return rts_chunk_count(tiles) * size_t(radix) * 8;
+}
+
+int os_rts_block_prefix(const unsigned int* counts, size_t tiles, int radix,
+                        unsigned long long* offsets, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  if (radix < 1 || radix > kMaxRadix || (radix & (radix - 1)) != 0)
+    return fail(OS_ERR_ARG, "radix must be a power of two <= %d", kMaxRadix);
+  if (tiles >= (size_t(1) << 32)) return fail(OS_ERR_ARG, "too many tiles");
+  if (tiles == 0) return OS_OK;
+  const size_t need = os_rts_prefix_workspace_bytes(tiles, radix);
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(OS_ERR_WORKSPACE, "rts prefix workspace needs %zu bytes, got %zu", need,
+                workspace_bytes);
+  OS_CUDA(launch_rts_prefix(counts, uint32_t(tiles), radix,
+                            static_cast<unsigned long long*>(workspace), offsets,
+                            static_cast<cudaStream_t>(stream)),
+          "rts prefix");
+  return OS_OK;
+}
+
+size_t os_rts_downsweep_workspace_bytes(void) { return 256; }
+
+int os_rts_downsweep(const void* src_keys, void* dst_keys, const void* src_vals, void* dst_vals,
+                     size_t n, int key_bytes, int val_bytes, int shift, int digit_width,
+                     const unsigned long long* offsets, int tile_keys, int codec_in,
+                     int codec_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if ((val_bytes == 0) != (src_vals == nullptr) || (val_bytes == 0) != (dst_vals == nullptr))
+    return fail(OS_ERR_ARG, "values pointers must be given iff val_bytes > 0");
+  if (digit_width < 1 || digit_width > kMaxDigitBits)
+    return fail(OS_ERR_ARG, "rts digit width must be in [1, %d]", kMaxDigitBits);
+  if (shift < 0 || shift >= key_bytes * 8) return fail(OS_ERR_ARG, "shift out of range");
+  if (codec_in < 0 || codec_in > 3 || codec_out < 0 || codec_out > 3)
+    return fail(OS_ERR_ARG, "bad codec");
+  const int cap = binning_tile_capacity(key_bytes, val_bytes);
+  if (tile_keys <= 0 || tile_keys > cap)
+    return fail(OS_ERR_ARG, "rts downsweep tile must be in [1, %d], got %d", cap, tile_keys);
+  if (n >= (size_t(1) << 32)) return fail(OS_ERR_ARG, "rts passes support n < 2^32");
+  if (n == 0) return OS_OK;
+  if (workspace == nullptr || workspace_bytes < os_rts_downsweep_workspace_bytes())
+    return fail(OS_ERR_WORKSPACE, "rts downsweep workspace needs %zu bytes",
+                os_rts_downsweep_workspace_bytes());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  OS_CUDA(cudaMemsetAsync(workspace, 0, 4, s), "tile ticket");
+  PassParams p{};
+  p.src_keys = src_keys;
+  p.dst_keys = dst_keys;
+  p.src_vals = src_vals;
+  p.dst_vals = dst_vals;
+  p.strip_n = uint32_t(n);
+  p.num_tiles = uint32_t((n + tile_keys - 1) / tile_keys);
+  p.tile_keys = uint32_t(tile_keys);
+  p.shift = shift;
+  p.radix = 1 << digit_width;
+  p.mask = uint32_t(p.radix - 1);
+  if (key_bytes == 4) {
+    const auto ci = XorCodec<uint32_t>::make(codec_in), co = XorCodec<uint32_t>::make(codec_out);
+    p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+  } else {
+    const auto ci = XorCodec<uint64_t>::make(codec_in), co = XorCodec<uint64_t>::make(codec_out);
+    p.cin_m0 = ci.m0, p.cin_m1 = ci.m1, p.cout_m0 = co.m0, p.cout_m1 = co.m1;
+  }
+  p.tile_counter = static_cast<uint32_t*>(workspace);
+  p.prefetch_tiles = prefetch_tiles();
+  p.wide_index = true;  // caller-provided 64-bit run starts
+  p.rts_offsets = offsets;
+  OS_CUDA(launch_binning_pass(p, key_bytes, val_bytes, s), "rts downsweep launch");
+  return OS_OK;
+}
+
 }  // extern "C"

@@ -2,8 +2,8 @@
 
 Mirrors onesweep.executor (executor.py:36-219).  On the GPU the thread pool is
 replaced by the CUDA grid (tile tickets are an atomicAdd in the binning
-kernel), so `Executor` keeps only what callers observe: the `workers`
-attribute (accepted and ignored), the optional `stream`, and the ledger.
+kernel); `Executor` keeps what callers observe -- `workers`, the optional
+`stream`, the ledger -- and `run_blocks` for host-driven blocks only.
 
 The ledger is filled analytically -- n element reads for the histogram,
 n reads + n writes per binning pass (binning.py:268-272) -- plus the
@@ -16,7 +16,9 @@ materialised lazily, so recording never forces a host synchronisation.
 from __future__ import annotations
 
 import os
+import random
 import threading
+import time
 from dataclasses import dataclass, field, replace
 
 _LEDGER_KINDS = (
@@ -77,17 +79,23 @@ class MemOpLedger:
 
 
 class Jitter:
-    """Accepted for signature compatibility (executor.py:108-121).
+    """Seeded random pauses around host-driven blocks (executor.py:108-121).
 
-    Block scheduling on the GPU is the hardware's; schedule exploration is done
-    by the device tests (reverse tile-claim pressure, many small tiles)."""
+    Device passes explore schedules with the debug library's in-kernel
+    __nanosleep jitter instead (tests/test_gpu_race.py)."""
 
     def __init__(self, seed: int = 0, max_pause_us: float = 50.0):
         self.seed = seed
         self.max_pause_us = max_pause_us
+        self._tls = threading.local()
 
-    def pause(self) -> None:  # pragma: no cover - nothing to pause on the host
-        return None
+    def pause(self) -> None:
+        """Sleep a seeded pseudo-random 0..max_pause_us (per-thread stream);
+        used by Executor.run_blocks around host-driven blocks."""
+        gen = getattr(self._tls, "gen", None)
+        if gen is None:
+            gen = self._tls.gen = random.Random(hash((self.seed, threading.get_ident())))
+        time.sleep(gen.random() * self.max_pause_us * 1e-6)
 
 
 class TileTicket:
@@ -128,6 +136,46 @@ class Executor:
         self.device_element_ops = 0
         self._pending: list[tuple[str, object, int]] = []  # (phase, device stats, radix)
         self._lock = threading.Lock()
+
+    def run_blocks(self, tiles: int, body) -> None:
+        """Host dispatch of body(tile) for tile in [0, tiles) on `workers`
+        threads (executor.py:160-212): ids come from one TileTicket in
+        increasing order, a thread finishes a block before drawing the next,
+        all threads are joined before returning, and the first failure is
+        re-raised (a real error in preference to a LookbackAborted it caused).
+        The device sort never calls this -- its blocks are the CUDA grid; it
+        serves callers that drive host-side blocks (process_tile)."""
+        if tiles <= 0:
+            return
+        ticket = TileTicket(tiles)
+        halt = threading.Event()
+        errors: list[BaseException] = []
+
+        def drain() -> None:
+            while not halt.is_set() and (tile := ticket.next_tile()) is not None:
+                try:
+                    if self.jitter is not None:
+                        self.jitter.pause()
+                    body(tile)
+                    if self.jitter is not None:
+                        self.jitter.pause()
+                except BaseException as exc:  # noqa: BLE001 - re-raised below
+                    errors.append(exc)
+                    halt.set()
+
+        if self.workers == 1:
+            drain()
+        else:
+            pool = [threading.Thread(target=drain, name=f"onesweep-block-{i}")
+                    for i in range(self.workers)]
+            for t in pool:
+                t.start()
+            for t in pool:
+                t.join()
+        if errors:
+            from .lookback import LookbackAborted
+
+            raise next((e for e in errors if not isinstance(e, LookbackAborted)), errors[0])
 
     def ledger_record(self, phase: str, kind: str, count: int) -> None:
         if kind not in _LEDGER_KINDS:

@@ -97,3 +97,77 @@ def test_rts_sort_above_one_strip(cuda):
     got = rts_sort(keys)
     want = torch.sort(keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, stable=True).values
     assert torch.equal(got.view(torch.int32).to(torch.int64) & 0xFFFFFFFF, want)
+
+
+@pytest.mark.parametrize("kb,d,tile,n", [(4, 8, 512, 20_000), (4, 3, 100, 3_001), (8, 5, 256, 9_000),
+                                          (4, 8, 4096, 4_096), (8, 8, 1000, 12_345)])
+def test_rts_building_blocks_match_oracle(cuda, kb, d, tile, n):
+    """rts_upsweep / rts_block_prefix / rts_downsweep on the device
+    (baseline.py:55-118) against numpy restatements of the reference's
+    formulas: per-tile bincount, digit-major exclusive scan, and the stable
+    partition (the oracle's partition pass with the same global offsets)."""
+    from oracle import oracle
+    from paper_2206_01784_b200 import (
+        BlockHistogramTable, Executor, radix_plan, rts_block_prefix, rts_downsweep, rts_upsweep)
+
+    rng = np.random.default_rng(n + d)
+    dt = np.uint32 if kb == 4 else np.uint64
+    keys = rng.integers(0, 2 ** (8 * kb), size=n, dtype=np.uint64).astype(dt)
+    cfg = radix_plan(8 * kb, d, tile_size=tile)
+    for place in (0, cfg.passes - 1):
+        shift = cfg.digit_shift(place)
+        digits = ((keys >> dt(shift)) & dt(cfg.radix - 1)).astype(np.int64)
+        tiles = -(-n // tile)
+        want = np.zeros((tiles, cfg.radix), np.int64)
+        for t in range(tiles):
+            want[t] = np.bincount(digits[t * tile:(t + 1) * tile], minlength=cfg.radix)
+        ex = Executor()
+        table = rts_upsweep(keys, place, cfg, ex)
+        assert isinstance(table, BlockHistogramTable)
+        assert np.array_equal(table.counts, want)
+        offsets = rts_block_prefix(table)
+        flat = want.T.reshape(-1)
+        want_off = (np.cumsum(flat) - flat).reshape(cfg.radix, tiles).T
+        assert np.array_equal(offsets, want_off)
+        out = np.zeros_like(keys)
+        vals = np.arange(n, dtype=np.uint64)
+        out_v = np.zeros_like(vals)
+        rts_downsweep(keys, place, offsets, out, cfg, ex, vals, out_v)
+        base = np.zeros(cfg.radix, np.uint64)
+        base[1:] = np.cumsum(want.sum(axis=0))[:-1]
+        ref_k, ref_v = np.zeros_like(keys), np.zeros_like(vals)
+        oracle.partition_pass(keys, ref_k, shift, d, base, vals, ref_v)
+        assert np.array_equal(out, ref_k) and np.array_equal(out_v, ref_v)
+        assert ex.ledger_snapshot().phase("upsweep").element_reads == n
+        assert ex.ledger_snapshot().phase("downsweep").element_writes == n
+
+
+def test_process_tile_chain_equals_partition_pass(cuda):
+    """Host-driven tiles (binning.py:162-215) through process_tile, chained
+    by a host CounterMatrix, place keys exactly as one device partition pass
+    and leave the reference's final counter words."""
+    from oracle import oracle
+    from paper_2206_01784_b200 import CounterMatrix, process_tile, radix_plan
+
+    rng = np.random.default_rng(5)
+    n, tile = 5_000, 700
+    cfg = radix_plan(32, 6, tile_size=tile)
+    keys = rng.integers(0, 2**32, size=n, dtype=np.uint32)
+    digits = (keys >> 6) & 63
+    base = np.zeros(64, np.uint64)
+    base[1:] = np.cumsum(np.bincount(digits, minlength=64))[:-1]
+    tiles = -(-n // tile)
+    m = CounterMatrix(tiles, cfg.radix)
+    out = np.zeros_like(keys)
+    carry = np.zeros(64, np.uint64)
+    fast = 0
+    for t in range(tiles):
+        stats = process_tile(t, keys[t * tile:(t + 1) * tile], out, 1, base, m, cfg,
+                             carry_out=carry if t == tiles - 1 else None)
+        fast += stats.fast_path_tiles
+        assert stats.element_reads == min(tile, n - t * tile)
+    want = np.zeros_like(keys)
+    _, _, words = oracle.partition_pass(keys, want, 6, 6, base, tile=tile, want_status=True)
+    assert np.array_equal(out, want)
+    assert np.array_equal(m.words.reshape(-1), words)
+    assert np.array_equal(carry, base + np.bincount(digits, minlength=64).astype(np.uint64))
