@@ -304,6 +304,132 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   }
 }
 
+// Specialisation for 64-bit keys with eight byte-aligned 8-bit places (C4).
+// Lane-private u32 counters would need 8 x 256 x 32 x 4 B = 256 KiB, so two
+// places share each counter word as u16 halves: word [place / 2][digit][lane],
+// half = place & 1.  The increment is then a compile-time constant per
+// (unrolled) place, and with the table 32 KiB-aligned one SHF + LOP3 turns a
+// key word straight into the counter address ((byte << 7) | pair base |
+// lane): three instructions per key and place, every red.shared
+// conflict-free (bank = lane).  A lane adds at most 2 * kHistVec keys per
+// round, so the u16 halves are folded into u32 block totals every
+// kU64FoldRounds rounds.
+constexpr size_t kHistU64Table = 4 * 256 * 32 * 4;                    // 128 KiB
+constexpr size_t kHistU64Smem = kHistU64Table + 32768 + 8 * 256 * 4;  // + alignment + totals
+constexpr int kU64FoldRounds = 65535 / (2 * kHistVec);
+
+template <bool CODED>
+__global__ void __launch_bounds__(kHistThreads, 1)
+    onesweep_histogram_u64d8_kernel(const HistParams P) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  __shared__ unsigned long long s_wsum[kHistWarps];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const uint32_t raw = smem_u32(s_raw);
+  const uint32_t tbase = (raw + 32767u) & ~32767u;  // counter table, 32 KiB-aligned
+  uint32_t* s_tab = reinterpret_cast<uint32_t*>(s_raw + (tbase - raw));
+  uint32_t* s_total = reinterpret_cast<uint32_t*>(s_raw + (tbase - raw) + kHistU64Table);
+  for (int i = tid; i < int(kHistU64Table / 4) + 8 * 256; i += kHistThreads) s_tab[i] = 0;
+  __syncthreads();
+  const XorCodec<uint64_t> codec = XorCodec<uint64_t>::make(P.codec);
+  const uint32_t lbase = tbase + uint32_t(lane) * 4u;
+  // one 32-bit half of a key: places 4*hi .. 4*hi+3, i.e. place pairs 2*hi, 2*hi+1
+  auto add_word = [&](uint32_t w, int hi) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t pb = lbase + uint32_t(2 * hi + (j >> 1)) * 32768u;
+      const uint32_t sh = j == 0 ? (w << 7) : (w >> (8 * j - 7));  // byte j at bits 7..14
+      uint32_t addr;
+      asm("lop3.b32 %0, %1, 0x7f80, %2, 0xea;" : "=r"(addr) : "r"(sh), "r"(pb));  // (a & b) | c
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"((j & 1) ? 0x10000u : 1u)
+                   : "memory");
+    }
+  };
+  auto add = [&](uint64_t x) {
+    if (CODED) x = codec(x);
+    add_word(uint32_t(x), 0);
+    add_word(uint32_t(x >> 32), 1);
+  };
+  auto fold = [&]() {
+    __syncthreads();
+    for (int b = tid; b < 8 * 256; b += kHistThreads) {
+      const int p = b >> 8, d = b & 255;
+      const uint32_t* w = s_tab + ((p >> 1) * 256 + d) * 32;
+      const int sh = (p & 1) * 16;
+      uint32_t sum = 0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) sum += (w[(l + lane) & 31] >> sh) & 0xffffu;
+      s_total[b] += sum;
+    }
+    __syncthreads();
+    for (int i = tid; i < int(kHistU64Table / 4); i += kHistThreads) s_tab[i] = 0;
+    __syncthreads();
+  };
+
+  const uint64_t* keys = static_cast<const uint64_t*>(P.keys);
+  const size_t n = P.n;
+  size_t head = ((16u - (reinterpret_cast<uintptr_t>(keys) & 15u)) & 15u) / 8;
+  if (head > n) head = n;
+  const size_t nvec = (n - head) / 2;
+  const size_t tail = head + nvec * 2;
+  const uint4* vp = reinterpret_cast<const uint4*>(keys + head);
+  const size_t stride = size_t(gridDim.x) * kHistThreads;
+  const size_t per_round = stride * kHistVec;
+  const size_t rounds = (nvec + per_round - 1) / per_round;  // same for every block
+  size_t v0 = size_t(blockIdx.x) * kHistThreads + tid;
+  uint4 cur[kHistVec];
+#pragma unroll
+  for (int u = 0; u < kHistVec; ++u)
+    if (v0 + u * stride < nvec) cur[u] = ld_stream_v4(vp + v0 + u * stride);
+  for (size_t r = 0; r < rounds; ++r) {
+    const size_t v1 = v0 + per_round;
+    uint4 nxt[kHistVec];
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)
+      if (v1 + u * stride < nvec) nxt[u] = ld_stream_v4(vp + v1 + u * stride);
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u)
+      if (v0 + u * stride < nvec) {
+        add((uint64_t(cur[u].y) << 32) | cur[u].x);
+        add((uint64_t(cur[u].w) << 32) | cur[u].z);
+      }
+#pragma unroll
+    for (int u = 0; u < kHistVec; ++u) cur[u] = nxt[u];
+    v0 = v1;
+    if ((r + 1) % kU64FoldRounds == 0) fold();
+  }
+  const size_t g = size_t(blockIdx.x) * kHistThreads + tid;
+  if (g < head) add(keys[g]);
+  if (tail + g < n) add(keys[tail + g]);
+  fold();
+  for (int b = tid; b < 8 * 256; b += kHistThreads)
+    if (s_total[b]) atomicAdd(&P.hist[b], (unsigned long long)s_total[b]);
+  if (P.offsets == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int p = 0; p < 8; ++p) {
+    const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
+    unsigned long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
+    if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
+    __syncthreads();
+  }
+}
+
 // Standalone per-row exclusive scan (one block per row, any radix).
 __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const unsigned long long* counts,
                                                               int radix,
@@ -380,6 +506,23 @@ static cudaError_t launch_hist_u32d8(const HistParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+#ifndef OS_HIST_U64D8
+#define OS_HIST_U64D8 1  // 0: 64-bit keys use the generic kernel
+#endif
+template <bool CODED>
+static cudaError_t launch_hist_u64d8(const HistParams& p, cudaStream_t stream) {
+  auto kern = onesweep_histogram_u64d8_kernel<CODED>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kHistU64Smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<hist_grid(), kHistThreads, kHistU64Smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_histogram(const HistParams& p, int key_bytes, cudaStream_t stream) {
   if (p.n == 0) return cudaSuccess;
   const bool full8 = p.digit_bits == 8 && p.top_bits == 8;
@@ -391,6 +534,10 @@ cudaError_t launch_histogram(const HistParams& p, int key_bytes, cudaStream_t st
     return launch_hist_t<uint32_t, 0>(p, stream);
   }
   if (key_bytes == 8) {
+    if (full8 && p.passes == 8 && p.begin_bit == 0 && OS_HIST_U64D8) {
+      if (p.codec != CODEC_NONE) return launch_hist_u64d8<true>(p, stream);
+      return launch_hist_u64d8<false>(p, stream);
+    }
     if (full8 && p.passes == 8) return launch_hist_t<uint64_t, 8>(p, stream);
     return launch_hist_t<uint64_t, 0>(p, stream);
   }
