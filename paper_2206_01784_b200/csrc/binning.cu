@@ -40,6 +40,7 @@
 // Keys move once in and once out: 2n element transfers per pass, the
 // reference's ledger identity (binning.py:268-272).
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -147,6 +148,15 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_RANK_ATOMIC
 #define OS_RANK_ATOMIC 0
 #endif
+// 1: one wave of resident blocks loops over the tiles (no per-tile block
+// launch); 0: one block per tile (each block still loops, claiming once more
+// to find the ticket exhausted)
+#ifndef OS_PERSIST
+#define OS_PERSIST 1
+#endif
+#ifndef OS_PERSIST_KEYS
+#define OS_PERSIST_KEYS 0  // u32 keys-only passes (see Geometry<4, 0>)
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
@@ -172,7 +182,7 @@ struct BinningSmem {
 };
 
 template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
-          bool BYTE>
+          bool BYTE, bool LOOP>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const PassParams P) {
   constexpr bool HAS_V = ValTraits<V>::kHas;
   constexpr int KB = sizeof(K);
@@ -246,17 +256,38 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   if (OS_PDL) grid_launch_dependents();  // the next pass may start its prologue
   if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
+  if (tid == 0) {
+    mbar_init(&s_bar_k, 1);
+    mbar_init(&s_bar_v, 1);
+    fence_mbar_init();
+  }
+  if (MAPPED) {
+    for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
+  }
+  if (STASH) tmem_fence_before_sync();
+  __syncthreads();
+  uint32_t taddr = 0;
+  if (STASH) {
+    tmem_fence_after_sync();
+    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * (ITEMS * NW + RW);
+  }
   // programmatic dependent launch: everything above overlaps the previous
   // pass's tail; its output (this pass's input) is complete after the wait
   if (OS_PDL) grid_dependency_wait();
+
+  // Tile loop.  The grid is at most one wave of resident blocks
+  // (launch_one), so a block takes tiles until the ticket runs past the
+  // strip: no block launch/retire gap between tiles, and the TMEM columns and
+  // barriers are set up once.  Tickets stay strictly increasing in claim
+  // order, and every claimed tile belongs to a running block (forward
+  // progress for the look-back).
+  uint32_t k_phase = 0, v_phase = 0;  // mbarrier phase parities
+  for (;;) {
   if (tid == 0) {
     const uint32_t t = atomicAdd(P.tile_counter, 1u);
     s_tile = t;
     s_fast = -1;
     s_reads = s_waits = s_rounds = 0;
-    mbar_init(&s_bar_k, 1);
-    mbar_init(&s_bar_v, 1);
-    fence_mbar_init();
     // warm L2 with a tile that a block starting a few microseconds from now
     // will claim; its TMA then hits L2 instead of waiting on HBM
     const uint32_t pf = t + P.prefetch_tiles;
@@ -276,18 +307,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     uint4* z = reinterpret_cast<uint4*>(s_whist);
     for (int i = tid; i < int(Smem::kHist / 16); i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
   }
-  if (MAPPED) {
-    for (int i = tid; i < kMaxRadix; i += THREADS) s_map[i] = P.digit_map[i];
-  }
-  if (STASH) tmem_fence_before_sync();
   __syncthreads();
-  uint32_t taddr = 0;
-  if (STASH) {
-    tmem_fence_after_sync();
-    taddr = s_tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(warp >> 2) * (ITEMS * NW + RW);
-  }
-
   const uint32_t tile = s_tile;
+  if (tile >= P.num_tiles) break;
   const uint32_t tile_start = tile * P.tile_keys;
   const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
   const bool full = valid == uint32_t(TILE);
@@ -336,7 +358,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (idx < valid) s_vals[idx] = gv[idx];
     }
   }
-  if (tma_k) mbar_wait_parity(&s_bar_k, 0);
+  if (tma_k) {
+    mbar_wait_parity(&s_bar_k, k_phase);
+    k_phase ^= 1u;
+  }
   asm volatile("" ::: "memory");  // the copies above before the (volatile) key loads below
   if (OS_TRACE && trace && tid == 0) trace[1] = global_ns();
 
@@ -565,7 +590,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   }
   VS vals[HAS_V && !STASH ? ITEMS : 1];
   if (HAS_V) {
-    if (tma_v) mbar_wait_parity(&s_bar_v, 0);
+    if (tma_v) {
+      mbar_wait_parity(&s_bar_v, v_phase);
+      v_phase ^= 1u;
+    }
     if constexpr (STASH) {  // values to the stash, next to the keys
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
@@ -693,9 +721,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       atomicAdd(&s_rounds, rounds);
     }
   }
-  if (STASH) tmem_fence_before_sync();
+  if (!LOOP && STASH) tmem_fence_before_sync();
   __syncthreads();
-  if (STASH && warp == 0) {
+  if (!LOOP && STASH && warp == 0) {  // one tile per block: free the columns early
     tmem_fence_after_sync();
     tmem_dealloc(s_tmem, TCOLS);
   }
@@ -749,15 +777,26 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     atomicAdd(&P.stats[3], (unsigned long long)s_waits);
     atomicAdd(&P.stats[4], (unsigned long long)s_rounds);
   }
+  if (!LOOP) break;
+  // the next tile's TMA (async proxy) overwrites the tile buffers this tile
+  // read and wrote through the generic proxy; the barrier at the top of the
+  // loop orders them after this fence
+  fence_proxy_async_smem();
+  if (STASH) tmem_fence_before_sync();
+  }  // tile loop
+  if (LOOP && STASH && warp == 0) {
+    tmem_fence_after_sync();
+    tmem_dealloc(s_tmem, TCOLS);
+  }
 }
 
 // ---- host side ------------------------------------------------------------------
 
 template <typename K, typename V, int THREADS, int ITEMS, int MINB, bool MAPPED, bool CODED,
-          bool BYTE>
+          bool BYTE, bool LOOP>
 static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
   using Smem = BinningSmem<THREADS, ITEMS, sizeof(K), ValTraits<V>::kBytes>;
-  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED, BYTE>;
+  auto kern = onesweep_binning_kernel<K, V, THREADS, ITEMS, MINB, MAPPED, CODED, BYTE, LOOP>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -766,9 +805,23 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     configured = true;
   }
   if (p.num_tiles == 0) return cudaSuccess;
+  // One wave: MINB blocks per SM, the residency every geometry is sized for
+  // (registers by the launch bounds, shared memory and TMEM columns by
+  // BinningSmem / TCOLS).  cudaOccupancyMaxActiveBlocksPerMultiprocessor
+  // reports 1 for these kernels, so it is not used.  A wave larger than what
+  // is resident would only leave blocks that start late and find the ticket
+  // exhausted.
+  static unsigned wave = 0;
+  if (wave == 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    wave = unsigned(sms * MINB);
+  }
+  const unsigned grid = LOOP ? (p.num_tiles < wave ? p.num_tiles : wave) : p.num_tiles;
   if (OS_PDL) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.num_tiles);
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = Smem::kBytes;
     cfg.stream = stream;
@@ -779,7 +832,7 @@ static cudaError_t launch_one(const PassParams& p, cudaStream_t stream) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
   }
-  kern<<<p.num_tiles, THREADS, Smem::kBytes, stream>>>(p);
+  kern<<<grid, THREADS, Smem::kBytes, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -797,9 +850,16 @@ template <int KB, int VB> struct Geometry;
 #ifndef OS_U32_MINB
 #define OS_U32_MINB 4
 #endif
-template <> struct Geometry<4, 0> { static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB; };
-template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; };
-template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; };
+// P: persistent tile loop (one wave of blocks) or one tile per block.  The
+// loop keeps its carried state in registers, which the 64-register keys-only
+// kernel cannot spare (spills: 734-765 vs 662 us/pass at C2); the key-value
+// kernels gain (C3 q=1 1086 -> 1071, q=16 906 -> 806, C4 1463 -> 1428 us/pass).
+template <> struct Geometry<4, 0> {
+  static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB;
+  static constexpr bool P = OS_PERSIST_KEYS;
+};
+template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; static constexpr bool P = OS_PERSIST; };
 #ifndef OS_P32_T
 #define OS_P32_T 256  // keys + values in TMEM, 3 blocks/SM: 1128 us/pass at q=1 (was 1222 at 2/SM)
 #define OS_P32_I 32
@@ -812,13 +872,13 @@ template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2;
 #define OS_K64_I 32
 #define OS_K64_B 2
 #endif
-template <> struct Geometry<4, 4> { static constexpr int T = OS_P32_T, I = OS_P32_I, B = OS_P32_B; };
-template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; };
-template <> struct Geometry<8, 0> { static constexpr int T = 512, I = 8, B = 2; };
-template <> struct Geometry<8, 1> { static constexpr int T = 512, I = 8, B = 2; };
-template <> struct Geometry<8, 2> { static constexpr int T = 512, I = 8, B = 2; };
-template <> struct Geometry<8, 4> { static constexpr int T = OS_K64_T, I = OS_K64_I, B = OS_K64_B; };
-template <> struct Geometry<8, 8> { static constexpr int T = 512, I = 8, B = 2; };
+template <> struct Geometry<4, 4> { static constexpr int T = OS_P32_T, I = OS_P32_I, B = OS_P32_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 0> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 1> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 2> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 4> { static constexpr int T = OS_K64_T, I = OS_K64_I, B = OS_K64_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 8> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
 
 template <typename K, typename V>
 static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
@@ -828,13 +888,13 @@ static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
   if (p.tile_keys == 0 || p.tile_keys > uint32_t(G::T * G::I)) return cudaErrorInvalidValue;
   const bool coded = (p.cin_m0 | p.cin_m1 | p.cout_m0 | p.cout_m1) != 0;
   const bool byte = (p.shift % 8) == 0 && p.mask == 0xffu;
-  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true, true, false>(p, stream);
+  if (p.digit_map != nullptr) return launch_one<K, V, G::T, G::I, G::B, true, true, false, G::P>(p, stream);
   if (coded) {
-    if (byte) return launch_one<K, V, G::T, G::I, G::B, false, true, true>(p, stream);
-    return launch_one<K, V, G::T, G::I, G::B, false, true, false>(p, stream);
+    if (byte) return launch_one<K, V, G::T, G::I, G::B, false, true, true, G::P>(p, stream);
+    return launch_one<K, V, G::T, G::I, G::B, false, true, false, G::P>(p, stream);
   }
-  if (byte) return launch_one<K, V, G::T, G::I, G::B, false, false, true>(p, stream);
-  return launch_one<K, V, G::T, G::I, G::B, false, false, false>(p, stream);
+  if (byte) return launch_one<K, V, G::T, G::I, G::B, false, false, true, G::P>(p, stream);
+  return launch_one<K, V, G::T, G::I, G::B, false, false, false, G::P>(p, stream);
 }
 
 template <typename K>

@@ -97,7 +97,7 @@ def main():
     cfgs.append(("C5 single-GPU 2^31 u32 keys (8 strips)", lambda: (
         generate_keys(KeyGenSpec(q=1, seed=0, n=1 << 31), device=dev), None, torch.uint32)))
     for name, make in cfgs:
-        if a.only and a.only not in name:
+        if a.only and not any(s in name for s in a.only.split(",")):
             continue
         keys, vals, dt = make()
         run(name, keys, vals, dt, a.steps, a.warmup)
