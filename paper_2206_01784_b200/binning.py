@@ -183,7 +183,7 @@ class DeviceSorter:
 
     def __init__(self, n: int, key_dtype, val_bytes: int = 0, digit_bits: int = 8,
                  begin_bit: int = 0, end_bit: int | None = None, tile_size: int = 0,
-                 strip_size: int = 0, device=None):
+                 strip_size: int = 0, device=None, graphs: bool = True):
         import torch
 
         self.spec = spec_for_dtype(key_dtype)
@@ -205,8 +205,10 @@ class DeviceSorter:
         self.device = torch.device(device or "cuda")
         self.ws = workspace(nbytes, self.device)
         self.stats = torch.zeros(5, dtype=torch.int64, device=self.device)
+        self.graphs = graphs
+        self._graphs: dict = {}  # call signature -> captured CUDA graph (None: seen once)
 
-    def __call__(self, keys, keys_out, values=None, values_out=None, stream=None, stats=True):
+    def _launch(self, keys, keys_out, values, values_out, stream, stats):
         _native.check(
             _native.load().os_sort(
                 _native.ptr(keys), _native.ptr(keys_out), _native.ptr(values),
@@ -216,6 +218,39 @@ class DeviceSorter:
                 _native.ptr(self.stats) if stats else None, _native.stream_handle(stream)),
             "onesweep_sort",
         )
+
+    def __call__(self, keys, keys_out, values=None, values_out=None, stream=None, stats=True):
+        """Sort on `stream` (default: the current stream).  With `graphs`
+        on, a repeat of the same call (same buffers, stream and stats flag)
+        replays the sort's launches as one CUDA graph: the kernels and their
+        order are identical, the per-launch gaps shrink (C1: 233 -> 220 us per
+        sort, tools/graph_probe.py).  The first call runs directly (and sets
+        the kernels' attributes), the second captures, later ones replay."""
+        if not self.graphs:
+            self._launch(keys, keys_out, values, values_out, stream, stats)
+            return keys_out if values is None else (keys_out, values_out)
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        key = (_native.ptr(keys), _native.ptr(keys_out), _native.ptr(values), _native.ptr(values_out),
+               st.cuda_stream, bool(stats))
+        g = self._graphs.get(key)
+        if g is None and key not in self._graphs:
+            if len(self._graphs) >= 8:  # a few buffer sets (SortPipeline rotates three)
+                self._graphs.pop(next(iter(self._graphs)))
+            self._graphs[key] = None  # seen once: run directly
+            self._launch(keys, keys_out, values, values_out, st, stats)
+        else:
+            if g is None:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(self.device)
+                side.wait_stream(st)
+                with torch.cuda.graph(g, stream=side):
+                    self._launch(keys, keys_out, values, values_out, side, stats)
+                st.wait_stream(side)
+                self._graphs[key] = g
+            with torch.cuda.stream(st):
+                g.replay()
         return keys_out if values is None else (keys_out, values_out)
 
 
