@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2206_01784_b200 import DeviceSorter, KeyGenSpec, generate_keys
-n = 1 << 28
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 28
 keys = generate_keys(KeyGenSpec(q=1, seed=0, n=n), device="cuda")
 out = torch.empty_like(keys)
 s = DeviceSorter(n, torch.uint32)

@@ -2,7 +2,7 @@
 
 Prints the distribution of each phase and how late predecessors publish L
 relative to a tile's look-back start -- the quantity that decides whether
-the decoupled look-back waits.  Usage: python tools/trace_diag.py [pass]"""
+the decoupled look-back waits.  Usage: python tools/trace_diag.py [pass] [n]"""
 import os
 import sys
 
@@ -13,10 +13,10 @@ import torch
 from paper_2206_01784_b200 import DeviceSorter, KeyGenSpec, _native, generate_keys
 
 pas = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-n = 1 << 28
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 28
 keys = generate_keys(KeyGenSpec(q=1, seed=0, n=n), device="cuda")
 out = torch.empty_like(keys)
-s = DeviceSorter(n, torch.uint32)
+s = DeviceSorter(n, torch.uint32, graphs=False)  # the trace pointer is set per launch
 for _ in range(3):
     s(keys, out, stats=False)
 tiles = (n + s.tile - 1) // s.tile
@@ -64,3 +64,12 @@ for i in range(1000, tiles, max(1, tiles // 4000)):
 q("distance to newest G at look-back start", np.array(dist, dtype=np.float64))
 rate = tiles / (dur / 1e3)
 print(f"tile rate {rate:.1f} tiles/us; resident blocks ~{np.mean([(claim <= x).sum() - (end <= x).sum() for x in np.linspace(dur*0.2, dur*0.8, 50)]):.0f}")
+
+
+# look-back duration by tile index: the first wave of resident blocks has no
+# published G below it, so its walks run back towards tile 0
+lb = gpub - reord
+wave = 148 * 4
+for lo, hi in ((0, wave // 4), (wave // 4, wave // 2), (wave // 2, wave), (wave, 2 * wave), (2 * wave, tiles)):
+    if lo < min(hi, tiles):
+        q(f"look-back, tiles [{lo},{min(hi, tiles)})", lb[lo:min(hi, tiles)])
