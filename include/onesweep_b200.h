@@ -89,6 +89,14 @@ int os_tile_capacity(int key_bytes, int val_bytes);
 int os_encode(const void* in, void* out, size_t n, int key_type, void* stream);
 int os_decode(const void* in, void* out, size_t n, int key_type, void* stream);
 
+/* dst[i] = src[index[i]] for rows of row_bytes bytes (any width), index
+ * u32 (index_bytes 4) or u64 (8).  Values wider than 8 bytes travel through
+ * the sort as an index payload and are gathered once at the end: the
+ * reference reorders values of any numpy dtype (binning.py:301-304,
+ * _kernels.py:85-128 scatter whole elements).  src and dst must not overlap. */
+int os_gather_rows(const void* src, const void* index, int index_bytes, void* dst, size_t n,
+                   size_t row_bytes, void* stream);
+
 /* Device restatement of keygen.generate_keys (keygen.py:46-76): key i (for
  * i = first_index .. first_index+n-1) is the AND of splitmix64 words at
  * counters i*q .. i*q+q-1, truncated to key_bits.  Bit-identical. */

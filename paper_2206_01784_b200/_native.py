@@ -39,6 +39,7 @@ SIGNATURES = {
     "os_tile_capacity": (_i, [_i, _i]),
     "os_encode": (_i, [_vp, _vp, _sz, _i, _vp]),
     "os_decode": (_i, [_vp, _vp, _sz, _i, _vp]),
+    "os_gather_rows": (_i, [_vp, _vp, _i, _vp, _sz, _sz, _vp]),
     "os_keygen": (_i, [_vp, _sz, _i, _i, _u64, _u64, _vp]),
     "os_histogram_workspace_bytes": (_sz, []),
     "os_histogram": (_i, [_vp, _sz, _i, _i, _i, _i, _i, _vp, _vp, _vp, _sz, _vp]),

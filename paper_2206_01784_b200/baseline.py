@@ -26,6 +26,7 @@ import numpy as np
 
 from . import _native
 from ._device import as_device, from_device, is_tensor, launch_on, workspace
+from ._values import _gather_rows, _index_payload, _payload_width, _rows_as, _val_bytes, _value_rows
 from .executor import Executor
 from .keycodec import MAX_DEVICE_DIGIT_BITS, radix_plan, spec_for_dtype
 
@@ -92,8 +93,12 @@ def rts_sort(keys, values=None, cfg=None, executor: Executor | None = None):
             return sk
         return sk, (values.clone() if is_tensor(values) else values.copy())
     dk, _ = as_device(keys)
-    dv = as_device(values)[0] if values is not None else None
-    vb = 0 if values is None else dv.element_size()
+    vb = _val_bytes(values)
+    wide = values is not None and not _payload_width(vb)
+    if wide:  # values wider than 8 bytes ride as an index payload
+        dv, vb = _index_payload(n, dk.device)
+    else:
+        dv = as_device(values)[0] if values is not None else None
     ok = torch.empty_like(dk)
     ov = torch.empty_like(dv) if dv is not None else None
     sorter = DeviceRtsSorter(n, dk.dtype, vb, device=dk.device)
@@ -109,6 +114,8 @@ def rts_sort(keys, values=None, cfg=None, executor: Executor | None = None):
     sk = from_device(ok, to_numpy)
     if values is None:
         return sk
+    if wide:
+        return sk, _rows_as(_gather_rows(_value_rows(values, dk.device), ov, vb), values, to_numpy)
     return sk, from_device(ov, to_numpy and not is_tensor(values))
 
 
@@ -247,6 +254,9 @@ def oracle_stable_sort(keys, values=None):
     if values is None:
         return sk
     vnp = not is_tensor(values)
+    if not _payload_width(_val_bytes(values)):  # e.g. complex128, structured dtypes
+        rows = _gather_rows(_value_rows(values, dk.device), order, 8)
+        return sk, _rows_as(rows, values, vnp)
     dv, _ = as_device(np.asarray(values) if vnp else values)
     return sk, from_device(_take(dv, order), vnp)
 

@@ -22,6 +22,7 @@ import numpy as np
 from . import _native
 from ._device import as_device, from_device, is_tensor, launch_on, workspace
 from .executor import Executor
+from ._values import _gather_rows, _index_payload, _payload_width, _rows_as, _val_bytes, _value_rows
 from .keycodec import MAX_DEVICE_DIGIT_BITS, RadixConfig, radix_plan, spec_for_dtype
 
 LANE_GROUP = 32
@@ -149,15 +150,6 @@ def short_circuit_check(ranking: TileRanking) -> int | None:
         return None
     top = int(np.argmax(ranking.digit_counts))
     return top if int(ranking.digit_counts[top]) == n else None
-
-
-def _val_bytes(values) -> int:
-    if values is None:
-        return 0
-    vb = values.element_size() if is_tensor(values) else values.dtype.itemsize
-    if vb not in (1, 2, 4, 8):
-        raise ValueError(f"values must be 1, 2, 4 or 8 bytes wide, got {vb}")
-    return vb
 
 
 def _numel(x) -> int:
@@ -294,7 +286,12 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     import torch
 
     dk, _ = as_device(keys)
-    dv = as_device(values)[0] if values is not None else None
+    wide = values is not None and not _payload_width(vb)
+    if wide:  # values ride as an index payload, gathered after the sort
+        wide_values = values
+        dv, vb = _index_payload(n, dk.device)
+    else:
+        dv = as_device(values)[0] if values is not None else None
     ok = torch.empty_like(dk)
     ov = torch.empty_like(dv) if dv is not None else None
     d = _device_digit_bits(cfg)
@@ -317,6 +314,9 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     sk = from_device(ok, to_numpy)
     if values is None:
         return sk
+    if wide:
+        rows = _gather_rows(_value_rows(wide_values, dk.device), ov, vb)
+        return sk, _rows_as(rows, wide_values, to_numpy)
     return sk, from_device(ov, to_numpy and not is_tensor(values))
 
 
@@ -346,7 +346,11 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
     dk, _ = as_device(dst_keys)
     sv = dv = None
     vb = _val_bytes(src_values)
-    if src_values is not None:
+    wide = src_values is not None and not _payload_width(vb)
+    if wide:  # values ride as an index payload, gathered after the pass
+        sv, vb = _index_payload(sk.numel(), sk.device)
+        dv = torch.empty_like(sv)
+    elif src_values is not None:
         sv, _ = as_device(src_values)
         dv, _ = as_device(dst_values)
     base = offsets.offsets if isinstance(offsets, StripCarry) else offsets
@@ -379,14 +383,20 @@ def partition_pass(src_keys, dst_keys, place: int, offsets, cfg: RadixConfig,
     executor.ledger_record("partition", "element_reads", n)
     executor.ledger_record("partition", "element_writes", n)
     executor.record_device_stats("partition", stats, cfg.radix)
+    if wide and dst_values is not None:
+        rows = _gather_rows(_value_rows(src_values, sk.device), dv, vb, executor.stream)
+        if is_tensor(dst_values):
+            dst_values.copy_(_rows_as(rows, dst_values, False))
+        else:
+            np.copyto(dst_values, _rows_as(rows, dst_values, True))
     if src_np or not is_tensor(dst_keys):
         np.copyto(dst_keys, dk.cpu().numpy().view(np.asarray(dst_keys).dtype))
-        if dst_values is not None:
+        if dst_values is not None and not wide:
             np.copyto(dst_values, dv.cpu().numpy().view(np.asarray(dst_values).dtype))
     else:
         if dk.data_ptr() != dst_keys.data_ptr():
             dst_keys.copy_(dk)
-        if dst_values is not None and dv.data_ptr() != dst_values.data_ptr():
+        if dst_values is not None and not wide and dv.data_ptr() != dst_values.data_ptr():
             dst_values.copy_(dv)
     result = StripCarry(carry.cpu().numpy() if carry_numpy else carry)
     if not return_status:

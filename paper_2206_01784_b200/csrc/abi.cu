@@ -293,6 +293,22 @@ int os_encode(const void* in, void* out, size_t n, int key_type, void* stream) {
   return OS_OK;
 }
 
+int os_gather_rows(const void* src, const void* index, int index_bytes, void* dst, size_t n,
+                   size_t row_bytes, void* stream) {
+  if (index_bytes != 4 && index_bytes != 8)
+    return fail(OS_ERR_ARG, "index_bytes must be 4 or 8, got %d", index_bytes);
+  if (n && (src == nullptr || index == nullptr || dst == nullptr))
+    return fail(OS_ERR_ARG, "null buffer");
+  if (n && row_bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src), b = reinterpret_cast<uintptr_t>(dst);
+    if (a < b + n * row_bytes && b < a + n * row_bytes) return fail(OS_ERR_ARG, "gather in place");
+  }
+  OS_CUDA(launch_gather_rows(src, index, index_bytes, dst, n, row_bytes,
+                             static_cast<cudaStream_t>(stream)),
+          "gather_rows");
+  return OS_OK;
+}
+
 int os_decode(const void* in, void* out, size_t n, int key_type, void* stream) {
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);

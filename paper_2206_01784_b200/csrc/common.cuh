@@ -541,6 +541,8 @@ cudaError_t launch_codec(const void* in, void* out, size_t n, int key_bytes, int
                          cudaStream_t stream);
 cudaError_t launch_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
                           unsigned long long first, cudaStream_t stream);
+cudaError_t launch_gather_rows(const void* src, const void* index, int index_bytes, void* dst,
+                               size_t n, size_t row_bytes, cudaStream_t stream);
 cudaError_t launch_rts_upsweep(const void* keys, size_t n, int key_bytes, uint32_t tile_keys,
                                int shift, uint32_t mask, int codec, uint32_t* counts,
                                cudaStream_t stream);

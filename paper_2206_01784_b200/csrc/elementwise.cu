@@ -83,3 +83,52 @@ cudaError_t launch_keygen(void* out, size_t n, int key_bits, int q, unsigned lon
 }
 
 }  // namespace osb
+
+namespace osb {
+
+// Row gather dst[i] = src[index[i]] for rows of row_bytes bytes: the value
+// payload of a sort whose values are wider than 8 bytes (onesweep_sort takes
+// any value dtype, binning.py:301-304) travels through the passes as a 4- or
+// 8-byte index and is gathered once at the end.  U is the widest unit that
+// divides the row and both base addresses; rows are cut into units and the
+// grid strides over (row, unit) pairs, so stores are coalesced.
+template <typename U, typename I>
+__global__ void gather_rows_kernel(const U* __restrict__ src, const I* __restrict__ index,
+                                   U* __restrict__ dst, size_t n, size_t units) {
+  const size_t total = n * units;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t u = size_t(blockIdx.x) * blockDim.x + threadIdx.x; u < total; u += stride) {
+    const size_t row = u / units, col = u - row * units;
+    dst[u] = src[size_t(index[row]) * units + col];
+  }
+}
+
+template <typename I>
+static cudaError_t gather_rows_typed(const void* src, const void* index, void* dst, size_t n,
+                                     size_t row_bytes, cudaStream_t stream) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | row_bytes;
+  const int threads = 256;
+  auto go = [&](auto unit) -> cudaError_t {
+    using U = decltype(unit);
+    const size_t units = row_bytes / sizeof(U);
+    const int grid = stream_grid(n * units, threads);
+    gather_rows_kernel<U, I><<<grid, threads, 0, stream>>>(
+        static_cast<const U*>(src), static_cast<const I*>(index), static_cast<U*>(dst), n, units);
+    return cudaGetLastError();
+  };
+  if ((a & 15u) == 0) return go(uint4{});
+  if ((a & 7u) == 0) return go(uint2{});
+  if ((a & 3u) == 0) return go(uint32_t{});
+  if ((a & 1u) == 0) return go(uint16_t{});
+  return go(uint8_t{});
+}
+
+cudaError_t launch_gather_rows(const void* src, const void* index, int index_bytes, void* dst,
+                               size_t n, size_t row_bytes, cudaStream_t stream) {
+  if (n == 0 || row_bytes == 0) return cudaSuccess;
+  if (index_bytes == 4) return gather_rows_typed<uint32_t>(src, index, dst, n, row_bytes, stream);
+  if (index_bytes == 8) return gather_rows_typed<unsigned long long>(src, index, dst, n, row_bytes, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace osb

@@ -193,3 +193,13 @@ def test_entropy_table():
 
     for q, want in {1: 1.0, 2: 0.811278, 3: 0.543564, 4: 0.33729, 8: 0.036875, 16: 0.000266}.items():
         assert expected_entropy(q) == pytest.approx(want, abs=5e-6)
+
+
+def test_gather_rows_argument_errors():
+    """os_gather_rows validates its arguments before touching the device."""
+    from paper_2206_01784_b200 import _native
+
+    L = _native.load()
+    assert L.os_gather_rows(None, None, 3, None, 0, 16, None) == _native.OS_ERR_ARG
+    assert L.os_gather_rows(None, None, 4, None, 10, 16, None) == _native.OS_ERR_ARG
+    assert L.os_gather_rows(None, None, 8, None, 0, 16, None) == _native.OS_OK  # empty: no-op
