@@ -157,6 +157,9 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_PERSIST_KEYS
 #define OS_PERSIST_KEYS 0  // u32 keys-only passes (see Geometry<4, 0>)
 #endif
+#ifndef OS_PAIR_STS
+#define OS_PAIR_STS 1
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
@@ -200,6 +203,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
                          (!HAS_V || VB == 4) && ITEMS % 8 == 0 && WARPS % 4 == 0;
   constexpr int KW = KB / 4;                 // TMEM words per key
   constexpr int NW = KW + (HAS_V ? 1 : 0);   // stashed words per item: key (+ value)
+  // u32 keys with u32 values, both stashed: the reorder writes (key, value)
+  // pairs into the key + value buffers viewed as one 8-byte-slot array (one
+  // STS.64 per item instead of two scattered STS.32), the run writes read
+  // them back with one LDS.64 (OS_PAIR_STS)
+  constexpr bool PAIRS = OS_PAIR_STS && STASH && KB == 4 && VB == 4 &&
+                         Smem::kKeys == size_t(TILE) * 4 && Smem::kVals == size_t(TILE) * 4;
   // packed ranks (two u16 per word) parked next to the keys, 4 words per store
   constexpr bool RSTASH = OS_RANK_STASH && STASH && !HAS_V && KW == 1 && ITEMS % 8 == 0;
   constexpr int RW = RSTASH ? ITEMS / 2 : 0;
@@ -631,6 +640,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         else
           off = lds_u16(fma_u32(digit(key), k_two, hbase));
         const uint32_t addr = fma_u32(off, k_one, fma_u32(r, k_one, slot0));
+        if constexpr (PAIRS) {  // slot s of the pair array at byte 8 s
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(fma_u32(addr - smem_base, k_two, smem_base)),
+                       "r"(uint32_t(key)), "r"(vc[i & 7]));
+          continue;
+        }
         sts_val(addr, key);
         if (HAS_V) {
           constexpr int kSh = log2i(KB);
@@ -746,6 +760,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     // ---- 5b. coalesced run writes: slot s of digit d lands at rel[d] + s ----
     // (output indices below 2^32: one 32-bit table entry per digit)
     auto write_slot = [&](uint32_t s) {
+      if constexpr (PAIRS) {
+        uint32_t x, v;
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(x), "=r"(v) : "r"(smem_base + s * 8u));
+        const uint32_t at = fma_u32(s_rel[digit(K(x))], k_one, s);
+        st_global_cs(reinterpret_cast<uint32_t*>(dst_k + at), uint32_t(CODED ? cout(K(x)) : K(x)));
+        st_global(reinterpret_cast<uint32_t*>(dst_v + at), v);
+        return;
+      }
       const K x = s_keys[s];
       const uint32_t at = fma_u32(s_rel[digit(x)], k_one, s);
       if constexpr (sizeof(K) == 4)
@@ -762,10 +784,20 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   } else {
     for (uint32_t s = tid; s < valid; s += THREADS) {
-      const K x = s_keys[s];
+      K x;
+      VS v{};
+      if constexpr (PAIRS) {
+        uint32_t a, b;
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(smem_base + s * 8u));
+        x = K(a);
+        v = VS(b);
+      } else {
+        x = s_keys[s];
+        if (HAS_V) v = s_vals[s];
+      }
       const unsigned long long at = s_ptr[digit(x)] + s;
       st_global(elem_at(dst_k, at), CODED ? cout(x) : x);
-      if (HAS_V) st_global(elem_at(dst_v, at), s_vals[s]);
+      if (HAS_V) st_global(elem_at(dst_v, at), v);
     }
   }
   if (OS_TRACE && trace && tid == 0) trace[5] = global_ns();
