@@ -160,6 +160,9 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_PAIR_STS
 #define OS_PAIR_STS 1
 #endif
+#ifndef OS_TMA_SLICES
+#define OS_TMA_SLICES 1
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
@@ -231,7 +234,12 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   __shared__ uint32_t s_tile;
   __shared__ int s_fast;
   __shared__ uint32_t s_reads, s_waits, s_rounds;
-  __shared__ __align__(8) uint64_t s_bar_k;
+  // key-arrival barriers: one per warp slice when the tile is staged in
+  // per-warp TMA slices (looping key-value kernels, OS_TMA_SLICES), so a
+  // warp starts ranking as soon as its own keys have landed
+  constexpr bool SLICE = OS_TMA_SLICES && LOOP;
+  constexpr int KBARS = SLICE ? WARPS : 1;
+  __shared__ __align__(8) uint64_t s_bar_k[KBARS];
   __shared__ __align__(8) uint64_t s_bar_v;
   __shared__ uint32_t s_tmem;
 
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   if (OS_PDL) grid_launch_dependents();  // the next pass may start its prologue
   if (STASH && warp == 0) tmem_alloc(&s_tmem, TCOLS);
   if (tid == 0) {
-    mbar_init(&s_bar_k, 1);
+    for (int b = 0; b < KBARS; ++b) mbar_init(&s_bar_k[b], 1);
     mbar_init(&s_bar_v, 1);
     fence_mbar_init();
   }
@@ -339,8 +347,18 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     tma_v = ((reinterpret_cast<uintptr_t>(gv) & 15u) == 0) && (((valid * sizeof(VS)) & 15u) == 0);
   if (tid == 0) {
     if (tma_k) {
-      mbar_arrive_expect_tx(&s_bar_k, valid * sizeof(K));
-      tma_bulk_g2s_hint(s_keys, gk, valid * sizeof(K), &s_bar_k, l2_policy_evict_first());
+      if (SLICE && full) {
+        constexpr uint32_t kSlice = uint32_t(ITEMS) * 32u * uint32_t(sizeof(K));
+        const uint64_t pol = l2_policy_evict_first();
+        for (int b = 0; b < KBARS; ++b) {
+          mbar_arrive_expect_tx(&s_bar_k[b], kSlice);
+          tma_bulk_g2s_hint(s_keys + b * ITEMS * 32, gk + b * ITEMS * 32, kSlice, &s_bar_k[b], pol);
+        }
+      } else {
+        mbar_arrive_expect_tx(&s_bar_k[0], valid * sizeof(K));
+        tma_bulk_g2s_hint(s_keys, gk, valid * sizeof(K), &s_bar_k[0], l2_policy_evict_first());
+        for (int b = 1; b < KBARS; ++b) mbar_arrive(&s_bar_k[b]);  // every barrier completes a phase
+      }
     }
     if (HAS_V && tma_v) {
       mbar_arrive_expect_tx(&s_bar_v, valid * sizeof(VS));
@@ -368,7 +386,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     }
   }
   if (tma_k) {
-    mbar_wait_parity(&s_bar_k, k_phase);
+    if (SLICE && full)
+      mbar_wait_parity(&s_bar_k[__shfl_sync(0xffffffffu, warp, 0)], k_phase);
+    else
+      mbar_wait_parity(&s_bar_k[0], k_phase);
     k_phase ^= 1u;
   }
   asm volatile("" ::: "memory");  // the copies above before the (volatile) key loads below
