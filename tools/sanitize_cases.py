@@ -91,6 +91,14 @@ def case_p2p_emulation():
     assert eq(got, want, np.uint32)
 
 
+def case_wide_values():
+    k = rng.integers(0, 1 << 12, size=20_000, dtype=np.uint32)
+    v = rng.standard_normal(k.size) + 1j * rng.standard_normal(k.size)  # complex128: gathered
+    gk, gv = onesweep_sort(k, v)
+    order = np.argsort(k, kind="stable")
+    assert np.array_equal(gk, k[order]) and np.array_equal(gv, v[order])
+
+
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
 for name in (sys.argv[1:] or list(CASES)):
     CASES[name]()
