@@ -210,10 +210,16 @@ def run_ours(args) -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        import datetime
+
+        # a stuck collective fails the run after 5 minutes instead of hanging
+        # it (NCCL async error handling aborts the communicator)
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        timeout = datetime.timedelta(seconds=300)
         if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+            dist.init_process_group("nccl", device_id=dev, timeout=timeout)
         else:
-            dist.init_process_group(args.backend)
+            dist.init_process_group(args.backend, timeout=timeout)
 
     from paper_2206_01784_b200 import DeviceSorter, KeyGenSpec, generate_keys, _native, onesweep_sort
 

@@ -8,8 +8,28 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/onesweep_b200.h"
 #include "common.cuh"
+
+// NVTX ranges around every launch (tracing): a
+// profiler timeline shows "onesweep histogram", "onesweep pass k", ... on
+// the host thread.  Header-only NVTX3; without an attached tool a push/pop
+// is a null-pointer check.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int k) {
+    char buf[48];
+    snprintf(buf, sizeof buf, fmt, k);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 namespace osb {
 int histogram_grid_size();
@@ -295,6 +315,7 @@ int os_encode(const void* in, void* out, size_t n, int key_type, void* stream) {
 
 int os_gather_rows(const void* src, const void* index, int index_bytes, void* dst, size_t n,
                    size_t row_bytes, void* stream) {
+  NvtxRange nvtx_range("onesweep gather_rows");
   if (index_bytes != 4 && index_bytes != 8)
     return fail(OS_ERR_ARG, "index_bytes must be 4 or 8, got %d", index_bytes);
   if (n && (src == nullptr || index == nullptr || dst == nullptr))
@@ -458,7 +479,10 @@ int wide_partition(const void* src_k, void* dst_k, const void* src_v, void* dst_
   hp.hist = u64(L.off_h8);
   hp.offsets = u64(L.off_o8);
   hp.done_counter = reinterpret_cast<unsigned int*>(ws + L.off_done);
-  OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  {
+    NvtxRange r("onesweep histogram");
+    OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  }
   // 2.-3. two stable binning sub-passes: low byte, then the high bits
   unsigned char* sub = ws + L.off_sub;
   uint32_t* status = reinterpret_cast<uint32_t*>(sub + L.pw.off_status);
@@ -515,6 +539,7 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
                       int codec_in, int codec_out, int tile_keys, size_t strip_keys,
                       unsigned int* status_out, void* workspace, size_t workspace_bytes,
                       os_device_stats* stats, void* stream) {
+  NvtxRange nvtx_range("onesweep partition_pass");
   if (key_bytes != 4 && key_bytes != 8) return fail(OS_ERR_ARG, "key_bytes must be 4 or 8");
   if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
   if ((val_bytes == 0) != (src_vals == nullptr) || (val_bytes == 0) != (dst_vals == nullptr))
@@ -646,7 +671,10 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
   hp.hist = hist;
   hp.offsets = offsets;
   hp.done_counter = reinterpret_cast<unsigned int*>(ws + L.off_done);
-  OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  {
+    NvtxRange r("onesweep histogram");
+    OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
+  }
   OS_CUDA(mark(1), "event");
 
   // Ping-pong so that the last pass lands in the caller's output buffer
@@ -666,6 +694,7 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
     unsigned long long* carry_final =
         reinterpret_cast<unsigned long long*>(pws + L.pw.off_carry) +
         (L.t.strips - 1) * size_t(L.radix);
+    NvtxRange r("onesweep pass %d", k);
     int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
                       offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
                       k == L.passes - 1 ? kt.dec : CODEC_NONE, status, nullptr, pws, L.pw,
@@ -710,6 +739,7 @@ int os_debug_trace(unsigned long long* buf, int pass) {
 
 int os_msd_histogram(const void* keys, size_t n, int key_type, int digit_bits, int end_bit,
                      unsigned long long* hist_out, void* stream) {
+  NvtxRange nvtx_range("onesweep msd_histogram");
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   if (int rc = check_bits(kt.bytes, digit_bits, end_bit - digit_bits, end_bit)) return rc;
@@ -756,6 +786,7 @@ int os_msd_partition(const void* keys_in, void* keys_out, const void* vals_in, v
                      const unsigned int* bin_lo, int parts,
                      const unsigned long long* seg_offsets, void* workspace,
                      size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range("onesweep msd_partition");
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
@@ -801,6 +832,7 @@ int os_msd_partition_p2p(const void* keys_in, void* keys_out, const void* vals_i
                          const unsigned int* bin_lo, int parts,
                          const unsigned long long* dest_index, void* workspace,
                          size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range("onesweep msd_partition_p2p");
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   if (val_bytes != 0 && val_bytes != kt.bytes)
@@ -882,6 +914,7 @@ size_t os_rts_sort_workspace_bytes(size_t n, int key_type, int val_bytes) {
 int os_rts_sort(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out, size_t n,
                 int key_type, int val_bytes, void* workspace, size_t workspace_bytes,
                 void** events, int num_events, void* stream) {
+  NvtxRange nvtx_range("onesweep rts_sort");
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");

@@ -272,11 +272,19 @@ def sharded_sort(keys, values=None, group=None, *, ops=None, digit_bits: int = S
     if values is not None and values.shape != keys.shape:
         raise ValueError("values must have the same length as keys")
 
+    phases = iter(("split", "exchange", "local"))
+
     def mark(name):
         if timings is not None and keys.is_cuda:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record()
             timings.append((name, ev))
+        if keys.is_cuda:  # NVTX range per phase on the profiler timeline
+            if name != "start":
+                torch.cuda.nvtx.range_pop()
+            nxt = next(phases, None)
+            if nxt is not None:
+                torch.cuda.nvtx.range_push(f"sharded_sort {nxt}")
 
     mark("start")
 
