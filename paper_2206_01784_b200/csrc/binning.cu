@@ -202,10 +202,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   using VS = typename std::conditional<HAS_V, V, uint32_t>::type;  // storage type
   constexpr int VB = HAS_V ? int(sizeof(VS)) : 0;
   // TMEM key stash: warp w owns lanes 32*(w%4).., columns (w/4)*ITEMS..
+  // Values of 1, 2 or 4 bytes take one TMEM column each (zero-extended),
+  // 8-byte values two, like 64-bit keys.
   constexpr bool STASH = OS_TMEM_STASH && (KB == 4 || (KB == 8 && OS_STASH64)) &&
-                         (!HAS_V || VB == 4) && ITEMS % 8 == 0 && WARPS % 4 == 0;
+                         (!HAS_V || VB <= 4 || (VB == 8 && OS_STASH64)) && ITEMS % 8 == 0 &&
+                         WARPS % 4 == 0;
   constexpr int KW = KB / 4;                 // TMEM words per key
-  constexpr int NW = KW + (HAS_V ? 1 : 0);   // stashed words per item: key (+ value)
+  constexpr int VW = HAS_V ? (VB == 8 ? 2 : 1) : 0;  // TMEM words per value
+  constexpr int NW = KW + VW;                // stashed words per item: key (+ value)
   // u32 keys with u32 values, both stashed: the reorder writes (key, value)
   // pairs into the key + value buffers viewed as one 8-byte-slot array (one
   // STS.64 per item instead of two scattered STS.32), the run writes read
@@ -627,8 +631,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     if constexpr (STASH) {  // values to the stash, next to the keys
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        kc[i & 7] = uint32_t(s_vals[warp_base + i * 32 + lane]);
-        if ((i & 7) == 7) tmem_st8(taddr + uint32_t(ITEMS * KW + i - 7), kc);
+        if constexpr (VW == 2) {
+          const uint64_t v = uint64_t(s_vals[warp_base + i * 32 + lane]);
+          kc[2 * (i & 3)] = uint32_t(v);
+          kc[2 * (i & 3) + 1] = uint32_t(v >> 32);
+          if ((i & 3) == 3) tmem_st8(taddr + uint32_t(ITEMS * KW + 2 * (i - 3)), kc);
+        } else {
+          kc[i & 7] = uint32_t(s_vals[warp_base + i * 32 + lane]);
+          if ((i & 7) == 7) tmem_st8(taddr + uint32_t(ITEMS * KW + i - 7), kc);
+        }
       }
       tmem_wait_st();
     } else {
@@ -647,7 +658,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        if (STASH && HAS_V && (i & 7) == 0) tmem_ld8(taddr + uint32_t(ITEMS * KW + i), vc);
+        if (STASH && HAS_V && VW == 1 && (i & 7) == 0) tmem_ld8(taddr + uint32_t(ITEMS * KW + i), vc);
+        if (STASH && HAS_V && VW == 2 && (i & 3) == 0) tmem_ld8(taddr + uint32_t(ITEMS * KW + 2 * i), vc);
         K key;
         if constexpr (STASH)
           key = unstash_key(i);
@@ -671,8 +683,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
           constexpr int kSh = log2i(KB);
           constexpr int vSh = log2i(VB > 0 ? VB : 1);
           const uint32_t slot = (addr - smem_base) >> kSh;
-          sts_val(smem_base + uint32_t(Smem::kKeys) + (slot << vSh),
-                  STASH ? VS(vc[i & 7]) : vals[STASH ? 0 : i]);
+          VS val;
+          if constexpr (STASH && VW == 2)
+            val = VS(uint64_t(vc[2 * (i & 3)]) | (uint64_t(vc[2 * (i & 3) + 1]) << 32));
+          else if constexpr (STASH)
+            val = VS(vc[i & 7]);
+          else
+            val = vals[i];
+          sts_val(smem_base + uint32_t(Smem::kKeys) + (slot << vSh), val);
         }
       }
     };
@@ -911,8 +929,36 @@ template <> struct Geometry<4, 0> {
   static constexpr int T = OS_U32_THREADS, I = OS_U32_ITEMS, B = OS_U32_MINB;
   static constexpr bool P = OS_PERSIST_KEYS;
 };
-template <> struct Geometry<4, 1> { static constexpr int T = 512, I = 16, B = 2; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2; static constexpr bool P = OS_PERSIST; };
+// Geometries of the other (key, value) widths, values stashed in TMEM like
+// C3/C4 (tools/value_widths.py, profiles/round2_binning_notes.md): 1.2-1.7x
+// the round-1 512-thread geometries.
+#ifndef OS_S32_T  // u32 keys with 1- or 2-byte values: 54.2 / 52.6 -> 66.6 / 63.7 GKey/s
+#define OS_S32_T 256
+#define OS_S32_I 32
+#define OS_S32_B 3
+#endif
+#ifndef OS_W32_T  // u32 keys with 8-byte values (numpy's int64 arange payload): 33.6 -> 46.2
+#define OS_W32_T 256
+#define OS_W32_I 32
+#define OS_W32_B 2
+#endif
+#ifndef OS_N64_T  // u64 keys, no values: 19.4 -> 32.2
+#define OS_N64_T 256
+#define OS_N64_I 32
+#define OS_N64_B 3
+#endif
+#ifndef OS_S64_T  // u64 keys with 1- or 2-byte values: 16.8 / 16.4 -> 24.5 / 23.8
+#define OS_S64_T 256
+#define OS_S64_I 32
+#define OS_S64_B 2
+#endif
+#ifndef OS_W64_T  // u64 keys with 8-byte values: 14.8 -> 18.4
+#define OS_W64_T 256
+#define OS_W64_I 24
+#define OS_W64_B 2
+#endif
+template <> struct Geometry<4, 1> { static constexpr int T = OS_S32_T, I = OS_S32_I, B = OS_S32_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<4, 2> { static constexpr int T = OS_S32_T, I = OS_S32_I, B = OS_S32_B; static constexpr bool P = OS_PERSIST; };
 #ifndef OS_P32_T
 #define OS_P32_T 256  // keys + values in TMEM, 3 blocks/SM: 1128 us/pass at q=1 (was 1222 at 2/SM)
 #define OS_P32_I 32
@@ -926,12 +972,12 @@ template <> struct Geometry<4, 2> { static constexpr int T = 512, I = 16, B = 2;
 #define OS_K64_B 2
 #endif
 template <> struct Geometry<4, 4> { static constexpr int T = OS_P32_T, I = OS_P32_I, B = OS_P32_B; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<4, 8> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<8, 0> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<8, 1> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<8, 2> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<4, 8> { static constexpr int T = OS_W32_T, I = OS_W32_I, B = OS_W32_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 0> { static constexpr int T = OS_N64_T, I = OS_N64_I, B = OS_N64_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 1> { static constexpr int T = OS_S64_T, I = OS_S64_I, B = OS_S64_B; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 2> { static constexpr int T = OS_S64_T, I = OS_S64_I, B = OS_S64_B; static constexpr bool P = OS_PERSIST; };
 template <> struct Geometry<8, 4> { static constexpr int T = OS_K64_T, I = OS_K64_I, B = OS_K64_B; static constexpr bool P = OS_PERSIST; };
-template <> struct Geometry<8, 8> { static constexpr int T = 512, I = 8, B = 2; static constexpr bool P = OS_PERSIST; };
+template <> struct Geometry<8, 8> { static constexpr int T = OS_W64_T, I = OS_W64_I, B = OS_W64_B; static constexpr bool P = OS_PERSIST; };
 
 template <typename K, typename V>
 static cudaError_t dispatch_geom(const PassParams& p, cudaStream_t stream) {
