@@ -957,7 +957,12 @@ template <> struct Geometry<4, 0> {
 #define OS_W64_I 24
 #define OS_W64_B 2
 #endif
-template <> struct Geometry<4, 1> { static constexpr int T = OS_S32_T, I = OS_S32_I, B = OS_S32_B; static constexpr bool P = OS_PERSIST; };
+#ifndef OS_B32_T  // u32 keys with 1-byte values: four blocks fit (66.6 -> 68.0 GKey/s)
+#define OS_B32_T 256
+#define OS_B32_I 32
+#define OS_B32_B 4
+#endif
+template <> struct Geometry<4, 1> { static constexpr int T = OS_B32_T, I = OS_B32_I, B = OS_B32_B; static constexpr bool P = OS_PERSIST; };
 template <> struct Geometry<4, 2> { static constexpr int T = OS_S32_T, I = OS_S32_I, B = OS_S32_B; static constexpr bool P = OS_PERSIST; };
 #ifndef OS_P32_T
 #define OS_P32_T 256  // keys + values in TMEM, 3 blocks/SM: 1128 us/pass at q=1 (was 1222 at 2/SM)
