@@ -13,6 +13,7 @@ import torch  # noqa: E402
 
 from oracle import oracle  # noqa: E402
 from paper_2206_01784_b200 import (  # noqa: E402
+    encode_array,
     global_histograms, onesweep_sort, partition_pass, radix_plan, rts_sort)
 from paper_2206_01784_b200.distributed import emulate_p2p_sort  # noqa: E402
 
@@ -97,6 +98,18 @@ def case_wide_values():
     gk, gv = onesweep_sort(k, v)
     order = np.argsort(k, kind="stable")
     assert np.array_equal(gk, k[order]) and np.array_equal(gv, v[order])
+
+
+def case_value_widths():
+    """every (key, value) width geometry: values stashed in TMEM (1/2/8 bytes)"""
+    for kdt in (np.uint32, np.int64):
+        k = rng.integers(0, 1 << 20, size=20_001).astype(kdt)
+        order = np.argsort(np.asarray(encode_array(k)), kind="stable")
+        assert np.array_equal(onesweep_sort(k).view(np.uint8), k[order].view(np.uint8))
+        for vdt in (np.uint8, np.int16, np.int64):
+            v = rng.integers(0, 1 << 7, size=k.size).astype(vdt)
+            gk, gv = onesweep_sort(k, v)
+            assert np.array_equal(gk.view(np.uint8), k[order].view(np.uint8)) and np.array_equal(gv, v[order])
 
 
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
