@@ -291,6 +291,19 @@ const char* os_version(void) {
 #endif
 }
 
+// Entry points whose first runtime call would be a kernel launch make one
+// plain runtime call first: when the library is loaded after the CUDA
+// context exists (torch initialised first), a launch as the very first
+// runtime call goes through an internal kernel-handle retry in cudart that
+// compute-sanitizer reports as an API error (the launch itself succeeds).
+static void runtime_ready() {
+  static bool ready = false;
+  if (!ready) {
+    cudaFree(nullptr);
+    ready = true;
+  }
+}
+
 int os_stream_check(void* stream) {
   // surfaces asynchronous kernel faults (a trapped look-back watchdog, an
   // illegal address) at the call that caused them
@@ -306,6 +319,7 @@ int os_tile_capacity(int key_bytes, int val_bytes) {
 }
 
 int os_encode(const void* in, void* out, size_t n, int key_type, void* stream) {
+  runtime_ready();
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   OS_CUDA(launch_codec(in, out, n, kt.bytes, kt.enc, static_cast<cudaStream_t>(stream)),
@@ -315,6 +329,7 @@ int os_encode(const void* in, void* out, size_t n, int key_type, void* stream) {
 
 int os_gather_rows(const void* src, const void* index, int index_bytes, void* dst, size_t n,
                    size_t row_bytes, void* stream) {
+  runtime_ready();
   NvtxRange nvtx_range("onesweep gather_rows");
   if (index_bytes != 4 && index_bytes != 8)
     return fail(OS_ERR_ARG, "index_bytes must be 4 or 8, got %d", index_bytes);
@@ -331,6 +346,7 @@ int os_gather_rows(const void* src, const void* index, int index_bytes, void* ds
 }
 
 int os_decode(const void* in, void* out, size_t n, int key_type, void* stream) {
+  runtime_ready();
   KeyType kt;
   if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
   OS_CUDA(launch_codec(in, out, n, kt.bytes, kt.dec, static_cast<cudaStream_t>(stream)),
@@ -340,6 +356,7 @@ int os_decode(const void* in, void* out, size_t n, int key_type, void* stream) {
 
 int os_keygen(void* out, size_t n, int key_bits, int q, unsigned long long seed,
               unsigned long long first_index, void* stream) {
+  runtime_ready();
   if (key_bits != 32 && key_bits != 64)
     return fail(OS_ERR_ARG, "key_bits must be 32 or 64, got %d", key_bits);
   if (q < 1) return fail(OS_ERR_ARG, "q must be >= 1, got %d", q);
