@@ -164,6 +164,17 @@ uint32_t prefetch_tiles() {
   return uint32_t(v);
 }
 
+// Device-side pass skipping in os_sort (plan_tickets); ONESWEEP_B200_NO_SKIP=1
+// turns it off (A/B runs; the reference's fixed (2p+1)n schedule).
+bool route_passes() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ONESWEEP_B200_NO_SKIP");
+    v = (e && atoi(e) != 0) ? 0 : 1;
+  }
+  return v != 0;
+}
+
 // Failure injection for the watchdog test (honoured by OS_JITTER builds
 // only): ONESWEEP_B200_DEBUG_STALL_TILE=t makes tile t of every pass skip its
 // status publishes, so its successors' look-backs must trap, not hang.
@@ -186,7 +197,8 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
              const unsigned long long* base0, unsigned long long* carry_final, int codec_in,
              int codec_out, uint32_t* status, uint32_t* tile_status, unsigned char* ws,
              const PassWs& w, unsigned long long* stats, cudaStream_t stream,
-             bool dense_bases, unsigned long long* trace = nullptr) {
+             bool dense_bases, unsigned long long* trace = nullptr,
+             const void* const* buf_keys = nullptr, const void* const* buf_vals = nullptr) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + w.off_counters);
   unsigned long long* carries = reinterpret_cast<unsigned long long*>(ws + w.off_carry);
   size_t tile_base = 0;
@@ -225,6 +237,17 @@ int run_pass(const void* src_k, void* dst_k, const void* src_v, void* dst_v, int
     p.wide_index = !dense_bases || t.n >= (size_t(1) << 32) - (size_t(1) << 26);
     p.trace = trace ? trace + tile_base * kTraceWords : nullptr;
     p.debug_stall_tile = debug_stall_tile();
+    if (buf_keys != nullptr) {  // routed sort pass: the ticket's route code picks a row
+      for (int ix = 0; ix < 8; ++ix) {
+        const int src = ix & 3;
+        if (src > 2) continue;
+        const int dst = (ix & 4) ? 2 : 1;  // output / workspace
+        p.route_bases[ix][0] = static_cast<const unsigned char*>(buf_keys[src]) + lo * kb;
+        p.route_bases[ix][1] = vb ? static_cast<const unsigned char*>(buf_vals[src]) + lo * vb : nullptr;
+        p.route_bases[ix][2] = buf_keys[dst];
+        p.route_bases[ix][3] = vb ? buf_vals[dst] : nullptr;
+      }
+    }
     OS_CUDA(launch_binning_pass(p, kb, vb, stream), "binning pass launch");
     base = p.carry_out;
     tile_base += p.num_tiles;
@@ -647,6 +670,7 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
   if (workspace == nullptr || workspace_bytes < L.total)
     return fail(OS_ERR_WORKSPACE, "sort workspace needs %zu bytes, got %zu", L.total,
                 workspace_bytes);
+  bool aliased = false;
   {
     // Aliasing: with an odd pass count pass 0 writes the caller's output while
     // other tiles still read the input, so no output may overlap any input.
@@ -658,10 +682,9 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
     const size_t kbytes = n * kb, vbytes = n * vb;
     if (overlap(keys_out, kbytes, vals_out, vbytes))
       return fail(OS_ERR_ARG, "keys_out and vals_out overlap");
-    if ((L.passes % 2) == 1 &&
-        (overlap(keys_out, kbytes, keys_in, kbytes) || overlap(keys_out, kbytes, vals_in, vbytes) ||
-         overlap(vals_out, vbytes, keys_in, kbytes) || overlap(vals_out, vbytes, vals_in, vbytes)))
-      return fail(OS_ERR_ARG, "in-place sort needs an even pass count");
+    aliased = overlap(keys_out, kbytes, keys_in, kbytes) || overlap(keys_out, kbytes, vals_in, vbytes) ||
+              overlap(vals_out, vbytes, keys_in, kbytes) || overlap(vals_out, vbytes, vals_in, vbytes);
+    if ((L.passes % 2) == 1 && aliased) return fail(OS_ERR_ARG, "in-place sort needs an even pass count");
   }
   if (n > size_t(osb::histogram_grid_size()) * (size_t(1) << 31))
     return fail(OS_ERR_ARG, "n too large");
@@ -688,6 +711,17 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
   hp.hist = hist;
   hp.offsets = offsets;
   hp.done_counter = reinterpret_cast<unsigned int*>(ws + L.off_done);
+  // Pass routing (plan_tickets): trivial places are skipped on the device,
+  // the plan rides in the tile tickets.  In-place sorts keep the fixed
+  // ping-pong (a skipped place would flip the parity and let a pass overwrite
+  // input it still reads), and so does ONESWEEP_B200_NO_SKIP=1.
+  const bool routed = !aliased && route_passes();
+  if (routed) {
+    hp.tickets = reinterpret_cast<uint32_t*>(ws + L.off_pass + L.pw.off_counters);
+    hp.ticket_stride = L.pw.bytes / sizeof(uint32_t);
+    hp.strips = int(L.t.strips);
+    hp.fixed_ends = kt.enc != CODEC_NONE;
+  }
   {
     NvtxRange r("onesweep histogram");
     OS_CUDA(launch_histogram(hp, kb, s), "histogram launch");
@@ -712,11 +746,16 @@ static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, v
         reinterpret_cast<unsigned long long*>(pws + L.pw.off_carry) +
         (L.t.strips - 1) * size_t(L.radix);
     NvtxRange r("onesweep pass %d", k);
+    // (coded keys: the first and last places always run, so the codec masks
+    // stay on pass 0 and the last pass, routed or not)
+    const void* buf_k[3] = {keys_in, tmp_k, keys_out};
+    const void* buf_v[3] = {vals_in, tmp_v, vals_out};
     int rc = run_pass(src_k, dst_k, src_v, dst_v, kb, vb, L.t, shift, width, L.radix, nullptr,
                       offsets + size_t(k) * L.radix, carry_final, k == 0 ? kt.enc : CODEC_NONE,
                       k == L.passes - 1 ? kt.dec : CODEC_NONE, status, nullptr, pws, L.pw,
                       reinterpret_cast<unsigned long long*>(stats), s, /*dense_bases=*/true,
-                      k == g_trace_pass ? g_trace : nullptr);
+                      k == g_trace_pass ? g_trace : nullptr, routed ? buf_k : nullptr,
+                      routed ? buf_v : nullptr);
     if (rc) return rc;
     OS_CUDA(mark(2 + k), "event");
     src_k = dst_k;

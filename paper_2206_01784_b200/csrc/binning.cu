@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   uint8_t* s_map = reinterpret_cast<uint8_t*>(s_wsum + 32);
 
   __shared__ uint32_t s_tile;
+  __shared__ const void* s_bases[4];  // tile's source keys / values, destination keys / values
+  uint32_t s_bases_code = ~0u;        // (thread 0) route code s_bases was resolved for
   __shared__ int s_fast;
   __shared__ uint32_t s_reads, s_waits, s_rounds;
   // key-arrival barriers: one per warp slice when the tile is staged in
@@ -253,8 +255,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   const int radix = P.radix;
   const int shift = P.shift;
   const uint32_t dmask = P.mask;
-  const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
-  const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
   // byte-aligned 8-bit digit: one PRMT picks it out of the right 32-bit word
   const uint32_t byte_sel = 0x4440u | uint32_t((shift & 31) >> 3);
   const bool hi_word = shift >= 32;
@@ -303,22 +303,37 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // order, and every claimed tile belongs to a running block (forward
   // progress for the look-back).
   uint32_t k_phase = 0, v_phase = 0;  // mbarrier phase parities
+  bool tmem_held = STASH;             // this block still owns its TMEM columns
   for (;;) {
   if (tid == 0) {
-    const uint32_t t = atomicAdd(P.tile_counter, 1u);
-    s_tile = t;
+    const uint32_t word = atomicAdd(P.tile_counter, 1u);  // ticket + route code (plan_tickets)
+    s_tile = word;
+    const uint32_t c = word >> kTicketShift;
+    if (c != s_bases_code) {  // this pass's buffer bases (the launch's own, or its route's)
+      s_bases_code = c;       // (the same for every tile of a pass: set at the first claim)
+      if (c == 0u || c == kTicketSkip) {
+        s_bases[0] = P.src_keys;
+        s_bases[1] = P.src_vals;
+        s_bases[2] = P.dst_keys;
+        s_bases[3] = P.dst_vals;
+      } else {
+        const uint32_t ix = (c - 1u) & 7u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s_bases[b] = P.route_bases[ix][b];
+      }
+    }
     s_fast = -1;
     s_reads = s_waits = s_rounds = 0;
     // warm L2 with a tile that a block starting a few microseconds from now
     // will claim; its TMA then hits L2 instead of waiting on HBM
-    const uint32_t pf = t + P.prefetch_tiles;
-    if (P.prefetch_tiles != 0 && pf + 1 < P.num_tiles) {
+    const uint32_t pf = (word & kTicketMask) + P.prefetch_tiles;
+    if (P.prefetch_tiles != 0 && pf + 1 < P.num_tiles && (word >> kTicketShift) != kTicketSkip) {
       const size_t off = size_t(pf) * P.tile_keys;
-      const K* pk = static_cast<const K*>(P.src_keys) + off;
+      const K* pk = static_cast<const K*>(s_bases[0]) + off;
       if ((reinterpret_cast<uintptr_t>(pk) & 15u) == 0 && ((P.tile_keys * KB) & 15u) == 0)
         l2_prefetch(pk, P.tile_keys * KB);
       if (HAS_V) {
-        const VS* pv = static_cast<const VS*>(P.src_vals) + off;
+        const VS* pv = static_cast<const VS*>(s_bases[1]) + off;
         if ((reinterpret_cast<uintptr_t>(pv) & 15u) == 0 && ((P.tile_keys * VB) & 15u) == 0)
           l2_prefetch(pv, P.tile_keys * VB);
       }
@@ -329,13 +344,22 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     for (int i = tid; i < int(Smem::kHist / 16); i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t code = s_tile >> kTicketShift;
+  const uint32_t tile = s_tile & kTicketMask;
+  if (code == kTicketSkip) {  // skipped place: every tile is a one-run tile (binning.py:201-205)
+    if (tile == 0 && tid == 0 && P.stats != nullptr) {
+      atomicAdd(&P.stats[0], (unsigned long long)P.num_tiles);
+      atomicAdd(&P.stats[2], (unsigned long long)P.num_tiles);
+    }
+    break;
+  }
   if (tile >= P.num_tiles) break;
+  const XorCodec<K> cin{K(P.cin_m0), K(P.cin_m1)};
   const uint32_t tile_start = tile * P.tile_keys;
   const uint32_t valid = min(P.tile_keys, P.strip_n - tile_start);
   const bool full = valid == uint32_t(TILE);
-  const K* gk = static_cast<const K*>(P.src_keys) + tile_start;
-  const VS* gv = HAS_V ? static_cast<const VS*>(P.src_vals) + tile_start : nullptr;
+  const K* gk = static_cast<const K*>(s_bases[0]) + tile_start;
+  const VS* gv = HAS_V ? static_cast<const VS*>(s_bases[1]) + tile_start : nullptr;
   unsigned long long* trace =
       (OS_TRACE && P.trace) ? P.trace + size_t(tile) * kTraceWords : nullptr;
   if (OS_TRACE && trace && tid == 0) {
@@ -774,15 +798,20 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       atomicAdd(&s_rounds, rounds);
     }
   }
+  // The destination is read before the barrier: after it, a looping block's
+  // thread 0 may claim the next tile (and rewrite s_tile / s_bases) while
+  // slower warps are still writing this one.
+  K* const dst_k = static_cast<K*>(const_cast<void*>(s_bases[2]));
+  VS* const dst_v = static_cast<VS*>(const_cast<void*>(s_bases[3]));
   if (!LOOP && STASH) tmem_fence_before_sync();
   __syncthreads();
   if (!LOOP && STASH && warp == 0) {  // one tile per block: free the columns early
     tmem_fence_after_sync();
     tmem_dealloc(s_tmem, TCOLS);
   }
+  tmem_held = LOOP;
 
-  K* const dst_k = static_cast<K*>(P.dst_keys);
-  VS* const dst_v = static_cast<VS*>(P.dst_vals);
+  const XorCodec<K> cout{K(P.cout_m0), K(P.cout_m1)};
   if (fast >= 0) {
     // ---- short circuit: homogeneous tile is one contiguous run --------------
     const unsigned long long base = s_ptr[fast];  // local start is 0
@@ -855,7 +884,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   fence_proxy_async_smem();
   if (STASH) tmem_fence_before_sync();
   }  // tile loop
-  if (LOOP && STASH && warp == 0) {
+  // (a one-tile block that met a skipped place or an exhausted ticket at
+  // its claim still holds its columns)
+  if (STASH && tmem_held && warp == 0) {
     tmem_fence_after_sync();
     tmem_dealloc(s_tmem, TCOLS);
   }

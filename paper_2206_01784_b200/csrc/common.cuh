@@ -475,6 +475,54 @@ __device__ __forceinline__ void grid_dependency_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// ---- pass routing (os_sort) --------------------------------------------------
+// A digit place whose histogram has one bin holding all n keys is an identity
+// permutation, so its pass can be skipped.  The upfront histogram's last
+// block decides this for every place and plans the remaining ping-pong so
+// that the last sorting pass still lands in the caller's output.  The plan
+// travels in the tile-ticket words themselves: the histogram initialises the
+// ticket of every (pass, strip) to code << kTicketShift, so the atomicAdd
+// that claims a tile also returns its pass's route (no extra load, no host
+// round trip, and the decision replays inside a CUDA graph).
+//   code 0           unrouted: the launch's own buffers and codec masks
+//   code kTicketSkip skipped place: the block exits at its first claim
+//   code 1 + bits    bits = src (0 input, 1 workspace, 2 output)
+//                           | 4 * (dst is the output) | 8 * first | 16 * last
+// For signed and float keys (a key codec on the first pass's loads and the
+// last pass's stores) the first and last places always run, so the codec
+// stays where the launches put it; only trivial places in between are
+// skipped.  first / last are informational.  If every place is trivial the
+// last place still runs, input to output: each tile takes the one-run fast
+// path, which is a copy.
+constexpr int kTicketShift = 27;
+constexpr uint32_t kTicketMask = (1u << kTicketShift) - 1u;
+constexpr uint32_t kTicketSkip = 31u;
+enum : uint32_t { kBufIn = 0, kBufTmp = 1, kBufOut = 2 };
+enum : uint32_t { kRouteDstOut = 4, kRouteFirst = 8, kRouteLast = 16 };
+__device__ __forceinline__ void plan_tickets(uint32_t* tickets, size_t pass_stride, int strips,
+                                             int passes, uint32_t trivial, bool fixed_ends) {
+  if (fixed_ends) trivial &= ~(1u | (1u << (passes - 1)));
+  int m = 0;
+  for (int k = 0; k < passes; ++k) m += ((trivial >> k) & 1u) ? 0 : 1;
+  if (m == 0) {  // all trivial: the last place runs as the copy
+    trivial &= ~(1u << (passes - 1));
+    m = 1;
+  }
+  int j = 0;
+  uint32_t cur = kBufIn;
+  for (int k = 0; k < passes; ++k) {
+    uint32_t code = kTicketSkip;
+    if (!((trivial >> k) & 1u)) {
+      const bool to_out = ((m - 1 - j) % 2) == 0;
+      code = 1u + (cur | (to_out ? kRouteDstOut : 0u) | (j == 0 ? kRouteFirst : 0u) |
+                   (j == m - 1 ? kRouteLast : 0u));
+      cur = to_out ? kBufOut : kBufTmp;
+      ++j;
+    }
+    for (int s = 0; s < strips; ++s) tickets[size_t(k) * pass_stride + s] = code << kTicketShift;
+  }
+}
+
 // ---- launch descriptors ------------------------------------------------------
 struct PassParams {
   const void* src_keys;  // strip-relative base already applied by the host
@@ -501,6 +549,11 @@ struct PassParams {
   uint32_t wide_index;                     // output indices may reach 2^32 (64-bit run writes)
   const unsigned long long* rts_offsets;   // reduce-then-scan ablation: [num_tiles][radix] run starts, or null
   int debug_stall_tile;                    // OS_JITTER builds: this tile never publishes (watchdog test); -1 off
+  // routed passes (ticket code > 0): buffer bases by route, index
+  // (code - 1) & 7 = src | 4 * (dst is the output); [0] source keys (this
+  // strip), [1] source values (this strip), [2] destination keys, [3]
+  // destination values (plan_tickets)
+  const void* route_bases[8][4];
 };
 // Per-tile trace record (globaltimer ns): claim, keys staged, L published,
 // reorder done, warp 0 G published, warp 0 done, SM id, unused.
@@ -527,6 +580,10 @@ struct HistParams {
   unsigned long long* hist;     // [passes][radix] (zeroed by host)
   unsigned long long* offsets;  // [passes][radix] or null
   unsigned int* done_counter;   // zeroed
+  uint32_t* tickets;            // [passes][strips] tile tickets of the routed passes, or null
+  size_t ticket_stride;         // words between two passes' tickets
+  int strips;
+  int fixed_ends;               // coded keys: the first and last places always run
 };
 
 // Host launchers (defined in the .cu files).

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
   extern __shared__ uint32_t s_hist[];  // [passes * radix/2][32] lane copies, then u32 totals
   __shared__ unsigned long long s_wsum[kHistWarps];
   __shared__ bool s_last;
+  __shared__ uint32_t s_trivial;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -178,13 +179,17 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
   // last-block-done: exclusive scan of each place (histogram.py:94-99)
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+    s_trivial = 0;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   for (int p = 0; p < P.passes; ++p) {
     const int i = tid;  // radix <= 256 < kHistThreads
     const unsigned long long x = (i < radix) ? __ldcg(&P.hist[p * radix + i]) : 0ull;
+    if (i < radix && x == P.n) atomicOr(&s_trivial, 1u << p);  // one bin holds every key
     unsigned long long incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
     if (i < radix) P.offsets[p * radix + i] = pre + incl - x;
     __syncthreads();
   }
+  if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, P.passes, s_trivial, P.fixed_ends != 0);
 }
 
 // Specialisation for the headline shape: 32-bit keys, four byte-aligned
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   extern __shared__ uint32_t s_cnt[];  // [place][digit][lane]
   __shared__ unsigned long long s_wsum[kHistWarps];
   __shared__ bool s_last;
+  __shared__ uint32_t s_trivial;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -283,12 +290,16 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   if (P.offsets == nullptr) return;
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+    s_trivial = 0;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   for (int p = 0; p < 4; ++p) {
     const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
+    if (tid < 256 && x == P.n) atomicOr(&s_trivial, 1u << p);  // one bin holds every key
     unsigned long long incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -302,6 +313,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
     __syncthreads();
   }
+  if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, 4, s_trivial, P.fixed_ends != 0);
 }
 
 // Specialisation for 64-bit keys with eight byte-aligned 8-bit places (C4).
@@ -324,6 +336,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ unsigned long long s_wsum[kHistWarps];
   __shared__ bool s_last;
+  __shared__ uint32_t s_trivial;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -409,12 +422,16 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   if (P.offsets == nullptr) return;
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    s_last = (atomicAdd(P.done_counter, 1u) == gridDim.x - 1);
+    s_trivial = 0;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   for (int p = 0; p < 8; ++p) {
     const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
+    if (tid < 256 && x == P.n) atomicOr(&s_trivial, 1u << p);  // one bin holds every key
     unsigned long long incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -428,6 +445,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
     __syncthreads();
   }
+  if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, 8, s_trivial, P.fixed_ends != 0);
 }
 
 // Standalone per-row exclusive scan (one block per row, any radix).
