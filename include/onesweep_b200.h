@@ -159,6 +159,18 @@ int os_partition_pass(const void* src_keys, void* dst_keys, const void* src_vals
  * stably sorted keys (native bit pattern) and their values.  vals_* may be
  * NULL (keys only; val_bytes must then be 0).  digit_bits <= 8.
  * tile_keys = 0 selects os_tile_capacity; strip_keys = 0 selects 2^28. */
+/* Copies, on `stream` after an os_sort with this workspace (and the same
+ * arguments), the first tile-ticket word of every pass to words[0..passes)
+ * (device or host memory; asynchronous for device memory).  A word whose top
+ * five bits (>> 27) are all ones marks a digit place that held every key in
+ * one bin, so the device skipped its pass (the route the upfront histogram
+ * planned into the tickets).  The reference runs every place
+ * (binning.py:313-326); its (2p+1)n ledger is the plan's, device element
+ * moves are (1 + 2 * passes run) n. */
+int os_sort_route_words(const void* workspace, size_t n, int key_type, int val_bytes,
+                        int digit_bits, int begin_bit, int end_bit, int tile_keys,
+                        size_t strip_keys, unsigned int* words, int max_passes, void* stream);
+
 size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_bits,
                                int begin_bit, int end_bit, int tile_keys,
                                size_t strip_keys);

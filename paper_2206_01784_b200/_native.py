@@ -50,6 +50,7 @@ SIGNATURES = {
     "os_partition_pass": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _sz,
                                _vp, _vp, _sz, _vp, _vp]),
     "os_sort_workspace_bytes": (_sz, [_sz, _i, _i, _i, _i, _i, _i, _sz]),
+    "os_sort_route_words": (_i, [_vp, _sz, _i, _i, _i, _i, _i, _i, _sz, _vp, _i, _vp]),
     "os_sort": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _i, _i, _sz, _vp, _sz, _vp, _vp]),
     "os_sort_events": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _i, _i, _sz, _vp, _sz, _vp,
                             ctypes.POINTER(_vp), _i, _vp]),

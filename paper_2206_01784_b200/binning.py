@@ -166,6 +166,11 @@ def _device_digit_bits(cfg: RadixConfig) -> int:
     return min(cfg.digit_bits, MAX_DEVICE_DIGIT_BITS)
 
 
+def skipped_from_route_words(words) -> list[bool]:
+    """Decode os_sort_route_words: top five bits all ones = skipped place."""
+    return [((int(w) & 0xFFFFFFFF) >> 27) == 31 for w in words.cpu().tolist()]
+
+
 class DeviceSorter:
     """Pre-planned device sort of n keys (optionally with values).
 
@@ -210,6 +215,26 @@ class DeviceSorter:
                 _native.ptr(self.stats) if stats else None, _native.stream_handle(stream)),
             "onesweep_sort",
         )
+
+    def route_words(self, stream=None):
+        """After a sort on `stream`: a device tensor with each pass's first
+        tile-ticket word (os_sort_route_words); asynchronous."""
+        import torch
+
+        words = torch.empty(self.passes, dtype=torch.int32, device=self.device)
+        _native.check(
+            _native.load().os_sort_route_words(
+                _native.ptr(self.ws), self.n, self.spec.type_id, self.val_bytes, self.digit_bits,
+                self.begin_bit, self.end_bit, self.tile, self.strip, _native.ptr(words), self.passes,
+                _native.stream_handle(stream)),
+            "route_words",
+        )
+        return words
+
+    def skipped_places(self, stream=None) -> list[bool]:
+        """After a sort on `stream`: which digit places held every key in one
+        bin and were skipped on the device (waits for the stream)."""
+        return skipped_from_route_words(self.route_words(stream))
 
     def __call__(self, keys, keys_out, values=None, values_out=None, stream=None, stats=True):
         """Sort on `stream` (default: the current stream).  With `graphs`
@@ -309,7 +334,9 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     executor.ledger_record("histogram", "element_reads", n)
     executor.ledger_record("partition", "element_reads", plan_passes * n)
     executor.ledger_record("partition", "element_writes", plan_passes * n)
-    executor.device_element_ops += (1 + 2 * sorter.passes) * n
+    # places the device skipped (one bin held every key) move no elements;
+    # the route words are copied now and decoded when the count is read
+    executor.record_device_route(n, sorter.route_words(stream if stream is not None else executor.stream))
     executor.record_device_stats("partition", sorter.stats, 1 << d)
     sk = from_device(ok, to_numpy)
     if values is None:

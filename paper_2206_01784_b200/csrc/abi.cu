@@ -641,6 +641,34 @@ size_t os_sort_workspace_bytes(size_t n, int key_type, int val_bytes, int digit_
   return sort_layout(n, kt.bytes, val_bytes, digit_bits, begin_bit, end_bit, tile, strip).total;
 }
 
+int os_sort_route_words(const void* workspace, size_t n, int key_type, int val_bytes,
+                        int digit_bits, int begin_bit, int end_bit, int tile_keys,
+                        size_t strip_keys, unsigned int* words, int max_passes, void* stream) {
+  KeyType kt;
+  if (!key_type_info(key_type, &kt)) return fail(OS_ERR_KEYTYPE, "unsupported key type %d", key_type);
+  if (!valid_val_bytes(val_bytes)) return fail(OS_ERR_ARG, "val_bytes must be 0/1/2/4/8");
+  if (int rc = check_bits(kt.bytes, digit_bits, begin_bit, end_bit)) return rc;
+  uint32_t tile;
+  size_t strip;
+  if (int rc = resolve_tile(tile_keys, kt.bytes, val_bytes, &tile)) return rc;
+  if (int rc = resolve_strip(strip_keys, &strip)) return rc;
+  const SortLayout L = sort_layout(n, kt.bytes, val_bytes, digit_bits, begin_bit, end_bit, tile, strip);
+  if (words == nullptr || max_passes < L.passes)
+    return fail(OS_ERR_ARG, "need room for %d passes", L.passes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n <= 1) {
+    OS_CUDA(cudaMemsetAsync(words, 0, size_t(L.passes) * sizeof(uint32_t), s), "route words");
+    return OS_OK;
+  }
+  if (workspace == nullptr) return fail(OS_ERR_WORKSPACE, "null workspace");
+  const unsigned char* ws = static_cast<const unsigned char*>(workspace);
+  for (int k = 0; k < L.passes; ++k)
+    OS_CUDA(cudaMemcpyAsync(words + k, ws + L.off_pass + size_t(k) * L.pw.bytes + L.pw.off_counters,
+                            sizeof(uint32_t), cudaMemcpyDefault, s),
+            "route words");
+  return OS_OK;
+}
+
 static int sort_impl(const void* keys_in, void* keys_out, const void* vals_in, void* vals_out,
                      size_t n, int key_type, int val_bytes, int digit_bits, int begin_bit,
                      int end_bit, int tile_keys, size_t strip_keys, void* workspace,

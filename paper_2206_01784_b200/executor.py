@@ -133,7 +133,8 @@ class Executor:
         self._ledger: dict[str, LedgerCounts] = {}
         # element reads + writes the device actually performed (equal to the
         # ledger's element_ops except when cfg.digit_bits > 8 runs as 8-bit places)
-        self.device_element_ops = 0
+        self._device_ops = 0
+        self._pending_routes: list[tuple[int, object]] = []  # (n, route words) of os_sort calls
         self._pending: list[tuple[str, object, int]] = []  # (phase, device stats, radix)
         self._lock = threading.Lock()
 
@@ -184,6 +185,31 @@ class Executor:
             counts = self._ledger.setdefault(phase, LedgerCounts())
             setattr(counts, kind, getattr(counts, kind) + int(count))
 
+    @property
+    def device_element_ops(self) -> int:
+        """Element reads + writes the device performed: the ledger's
+        element_ops, except for places the device skipped (one bin held every
+        key) and cfg.digit_bits > 8 plans run as 8-bit places."""
+        with self._lock:
+            pending, self._pending_routes = self._pending_routes, []
+        for n, words in pending:
+            from .binning import skipped_from_route_words
+
+            skipped = skipped_from_route_words(words)
+            self._device_ops += (1 + 2 * (len(skipped) - sum(skipped))) * n
+        return self._device_ops
+
+    @device_element_ops.setter
+    def device_element_ops(self, value: int) -> None:
+        with self._lock:
+            self._pending_routes = []
+        self._device_ops = int(value)
+
+    def record_device_route(self, n: int, words) -> None:
+        """Queue the route words of an os_sort of n keys (see device_element_ops)."""
+        with self._lock:
+            self._pending_routes.append((int(n), words))
+
     def record_device_stats(self, phase: str, stats, radix: int) -> None:
         """Queue an os_device_stats tensor [fast_tiles, lookback_reads, tiles]."""
         with self._lock:
@@ -206,7 +232,8 @@ class Executor:
         with self._lock:
             self._ledger.clear()
             self._pending.clear()
-            self.device_element_ops = 0
+            self._pending_routes.clear()
+            self._device_ops = 0
 
 
 def ledger_as_row(ledger: MemOpLedger) -> dict[str, int]:

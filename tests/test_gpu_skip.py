@@ -117,3 +117,29 @@ def test_no_skip_switch_gives_same_bytes(cuda, tmp_path):
         subprocess.run([sys.executable, "-c", code, str(out)], check=True, env=env, cwd=ROOT)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_skipped_places_reported(cuda):
+    """DeviceSorter.skipped_places / os_sort_skipped_places and the device
+    element count of the ledger follow the plan"""
+    import torch
+
+    from paper_2206_01784_b200 import DeviceSorter, Executor, onesweep_sort
+
+    r = np.random.default_rng(5)
+    n = 60_000
+    cases = [
+        (r.integers(0, 1 << 16, n).astype(np.uint32), [False, False, True, True]),
+        (np.full(n, 9, np.uint32), [True, True, True, False]),  # the last place runs as the copy
+        (r.integers(0, 1 << 20, n).astype(np.int64), [False, False, False, True, True, True, True, False]),
+        (r.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32), [False] * 4),
+    ]
+    for keys, want in cases:
+        t = torch.from_numpy(keys).cuda()
+        s = DeviceSorter(n, t.dtype, graphs=False)
+        out = torch.empty_like(t)
+        s(t, out)
+        assert s.skipped_places() == want, (keys.dtype, want)
+        ex = Executor()
+        onesweep_sort(keys, executor=ex)
+        assert ex.device_element_ops == (1 + 2 * (len(want) - sum(want))) * n
