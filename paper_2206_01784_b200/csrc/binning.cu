@@ -163,6 +163,9 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_TMA_SLICES
 #define OS_TMA_SLICES 1
 #endif
+#ifndef OS_KEEP_COUNTS
+#define OS_KEEP_COUNTS 1  // the count phase keeps the per-warp counts in registers for the offset rewrite
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
@@ -596,10 +599,23 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
+  // per-warp counts of this thread's digit, two u16 per register, kept for
+  // the offset rewrite below (OS_KEEP_COUNTS; else re-read)
+  constexpr bool KEEPC = OS_KEEP_COUNTS && kCounterBytes == 2;
+  uint32_t cpk[KEEPC ? (WARPS + 1) / 2 : 1];
   if (tid < radix) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) sum += s_whist[w * kMaxRadix + tid];
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = s_whist[w * kMaxRadix + tid];
+      sum += c;
+      if constexpr (KEEPC) {
+        if (w & 1)
+          cpk[w / 2] |= c << 16;
+        else
+          cpk[w / 2] = c;
+      }
+    }
     count = sum / KB;
     if (tid == radix - 1) count -= uint32_t(TILE) - valid;
     if (P.rts_offsets == nullptr) {  // (reduce-then-scan passes have no look-back)
@@ -631,8 +647,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     // needs a single shared-memory gather per key
     uint32_t run = local_start * KB;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) {  // counts re-read: registers are scarce here
-      const uint32_t c = s_whist[w * kMaxRadix + tid];
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = KEEPC ? ((cpk[w / 2] >> (16 * (w & 1))) & 0xffffu) : uint32_t(s_whist[w * kMaxRadix + tid]);
       s_whist[w * kMaxRadix + tid] = CT(run);
       run += c;
     }
