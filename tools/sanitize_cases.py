@@ -112,6 +112,21 @@ def case_value_widths():
             assert np.array_equal(gk.view(np.uint8), k[order].view(np.uint8)) and np.array_equal(gv, v[order])
 
 
+def case_skipped_places():
+    """device-side pass skipping: small-range keys (two places skipped), all-equal pairs
+    (every place but the last skipped), small signed 64-bit keys (middle places skipped)"""
+    k = rng.integers(0, 1 << 16, size=30_001).astype(np.uint32)
+    assert np.array_equal(onesweep_sort(k), np.sort(k, kind="stable"))
+    eq = np.full(25_000, 0x1234, np.uint32)
+    v = np.arange(eq.size, dtype=np.uint32)
+    gk, gv = onesweep_sort(eq, v)
+    assert np.array_equal(gk, eq) and np.array_equal(gv, v)
+    s = rng.integers(-(1 << 20), 1 << 20, size=20_000).astype(np.int64)
+    gk, gv = onesweep_sort(s, v[:s.size])
+    order = np.argsort(s, kind="stable")
+    assert np.array_equal(gk, s[order]) and np.array_equal(gv, v[:s.size][order])
+
+
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
 for name in (sys.argv[1:] or list(CASES)):
     CASES[name]()
