@@ -166,6 +166,9 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_KEEP_COUNTS
 #define OS_KEEP_COUNTS 1  // the count phase keeps the per-warp counts in registers for the offset rewrite
 #endif
+#ifndef OS_COUNT_PAIRS
+#define OS_COUNT_PAIRS 1  // the count phase works on digit pairs (one 32-bit counter word per thread)
+#endif
 #ifndef OS_KEY_PREFETCH
 #define OS_KEY_PREFETCH 2  // k: the ranking loop loads item i+k's key while ranking item i (C2: k=0 686, 1 659, 2 657 us/pass)
 #endif
@@ -213,6 +216,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   constexpr int KW = KB / 4;                 // TMEM words per key
   constexpr int VW = HAS_V ? (VB == 8 ? 2 : 1) : 0;  // TMEM words per value
   constexpr int NW = KW + VW;                // stashed words per item: key (+ value)
+  constexpr bool CPAIRS = OS_COUNT_PAIRS && kCounterBytes == 2 && THREADS * 2 >= kMaxRadix &&
+                         TILE * KB < 65536;  // (a digit's packed tile total must stay below 2^16)
   // u32 keys with u32 values, both stashed: the reorder writes (key, value)
   // pairs into the key + value buffers viewed as one 8-byte-slot array (one
   // STS.64 per item instead of two scattered STS.32), the run writes read
@@ -599,6 +604,69 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 
   // ---- 4a. tile counts, publish L, local digit starts ------------------------
   uint32_t count = 0;
+  uint32_t local_start = 0;
+  if constexpr (CPAIRS) {
+    // Digit pairs (OS_COUNT_PAIRS): thread t < ceil(radix / 2) owns digits 2t
+    // and 2t + 1, which share one 32-bit word of every per-warp counter
+    // table (u16 halves, each at most 40960 = tile x key width, so packed
+    // sums and offsets never carry across the halves): half the shared
+    // loads and stores of one thread per digit, and half the scan.  Each
+    // digit's (count, local start) goes to s_local for its look-back thread.
+    const int d0 = 2 * tid, d1 = 2 * tid + 1;
+    const bool owner = d0 < radix, has1 = d1 < radix;
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(s_whist);
+    uint32_t wk[WARPS];
+    uint32_t c0 = 0, c1 = 0;
+    if (owner) {
+      uint32_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        wk[w] = w32[w * (kMaxRadix / 2) + tid];
+        sum += wk[w];
+      }
+      c0 = (sum & 0xffffu) / KB;
+      c1 = (sum >> 16) / KB;
+      if (d0 == radix - 1) c0 -= uint32_t(TILE) - valid;
+      if (d1 == radix - 1) c1 -= uint32_t(TILE) - valid;
+      if (P.rts_offsets == nullptr) {  // (reduce-then-scan passes have no look-back)
+        const uint32_t flag = tile == 0 ? kFlagGlobal : kFlagLocal;
+        if (OS_JITTER) jitter_sleep(tile, d0, 1);
+        if (!OS_JITTER || int(tile) != P.debug_stall_tile) {
+          status_st(P.status + size_t(tile) * radix + d0, flag | c0);
+          if (has1) status_st(P.status + size_t(tile) * radix + d1, flag | c1);
+        }
+      }
+      if (c0 == valid) s_fast = d0;
+      if (has1 && c1 == valid) s_fast = d1;
+    }
+    if (OS_TRACE && trace && tid == 0) trace[2] = global_ns();
+    const uint32_t pair = c0 + c1;
+    uint32_t incl = pair;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31 && warp < kMaxRadix / 64) s_wsum[warp] = incl;
+    __syncthreads();
+    if (owner) {
+      uint32_t wpre = 0;
+#pragma unroll
+      for (int w = 0; w < kMaxRadix / 64; ++w) wpre += (w < warp) ? s_wsum[w] : 0u;
+      const uint32_t ls0 = wpre + incl - pair, ls1 = ls0 + c0;
+      s_local[d0] = ls0 | (c0 << 16);  // (counts and starts are below 2^16)
+      if (has1) s_local[d1] = ls1 | (c1 << 16);
+      // fold the tile-local starts into every warp's counters, so the
+      // reorder needs a single shared-memory gather per key
+      uint32_t run = (ls0 * KB) | ((ls1 * KB) << 16);
+      uint32_t* o32 = reinterpret_cast<uint32_t*>(s_whist);
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        o32[w * (kMaxRadix / 2) + tid] = run;
+        run += wk[w];
+      }
+    }
+  } else {
   // per-warp counts of this thread's digit, two u16 per register, kept for
   // the offset rewrite below (OS_KEEP_COUNTS; else re-read)
   constexpr bool KEEPC = OS_KEEP_COUNTS && kCounterBytes == 2;
@@ -636,7 +704,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   }
   if (lane == 31 && warp < kMaxRadix / 32) s_wsum[warp] = incl;
   __syncthreads();
-  uint32_t local_start = 0;
   if (tid < radix) {
     uint32_t wpre = 0;
 #pragma unroll
@@ -652,6 +719,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       s_whist[w * kMaxRadix + tid] = CT(run);
       run += c;
     }
+  }
   }
   // keys and values into registers; after the barrier the tile buffers are
   // rewritten in place as per-digit runs
@@ -746,6 +814,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   // re-poll a predecessor that has not published yet.  Then publish G and the
   // per-digit output indices.
   if (tid < radix) {
+    if constexpr (CPAIRS) {  // this digit's (count, local start) from the count phase
+      const uint32_t cl = s_local[tid];
+      count = cl >> 16;
+      local_start = cl & 0xffffu;
+    }
     uint32_t excl = 0;
     uint32_t reads = 0, waits = 0, rounds = 0;
     if (OS_JITTER) jitter_sleep(tile, tid, 2);
