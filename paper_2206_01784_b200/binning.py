@@ -334,6 +334,12 @@ def onesweep_sort(keys, values=None, cfg: RadixConfig | None = None,
     executor.ledger_record("histogram", "element_reads", n)
     executor.ledger_record("partition", "element_reads", plan_passes * n)
     executor.ledger_record("partition", "element_writes", plan_passes * n)
+    if plan_passes % 2 == 1:
+        # the reference's plan delivers an odd pass count with a parity copy,
+        # its own ledger line (binning.py:327-334); the device routes the
+        # passes so the last one writes the output and copies nothing, which
+        # device_element_ops records
+        executor.ledger_record("copy", "copy_ops", 2 * n)
     # places the device skipped (one bin held every key) move no elements;
     # the route words are copied now and decoded when the count is read
     executor.record_device_route(n, sorter.route_words(stream if stream is not None else executor.stream))

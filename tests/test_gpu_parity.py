@@ -217,8 +217,10 @@ def test_distributions_match_reference(cuda, golden, tag):
 
 def test_odd_pass_count_avoids_parity_copy(cuda, golden):
     # d=7 -> 5 passes.  The reference ledgers 11n + a 2n parity copy
-    # (test_binning.py:353-362); the device routes the passes so the last one
-    # lands in the output buffer, so the copy never happens.
+    # (test_binning.py:353-362) and so does the plan's ledger here; the device
+    # routes the passes so the last one lands in the output buffer, so the
+    # copy never happens on the device (device_element_ops: five 7-bit passes,
+    # (2*5+1)n, no copy).
     from paper_2206_01784_b200 import Executor, onesweep_sort, radix_plan
 
     keys = golden["odd_in"]
@@ -227,7 +229,8 @@ def test_odd_pass_count_avoids_parity_copy(cuda, golden):
     assert np.array_equal(got, golden["odd_keys"])
     snap = ex.ledger_snapshot()
     assert snap.element_ops == int(golden["odd_ledger"][0]) == 11 * keys.size
-    assert snap.copy_ops == 0
+    assert snap.copy_ops == 2 * keys.size
+    assert ex.device_element_ops == 11 * keys.size
 
 
 def test_sort_rejects_bad_arguments(cuda):
