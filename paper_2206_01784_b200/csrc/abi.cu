@@ -656,8 +656,10 @@ int os_sort_route_words(const void* workspace, size_t n, int key_type, int val_b
   if (words == nullptr || max_passes < L.passes)
     return fail(OS_ERR_ARG, "need room for %d passes", L.passes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (n <= 1) {
-    OS_CUDA(cudaMemsetAsync(words, 0, size_t(L.passes) * sizeof(uint32_t), s), "route words");
+  if (n <= 1) {  // nothing ran: no place skipped (words may be host or device memory)
+    static const uint32_t zeros[64] = {};
+    OS_CUDA(cudaMemcpyAsync(words, zeros, size_t(L.passes) * sizeof(uint32_t), cudaMemcpyDefault, s),
+            "route words");
     return OS_OK;
   }
   if (workspace == nullptr) return fail(OS_ERR_WORKSPACE, "null workspace");
