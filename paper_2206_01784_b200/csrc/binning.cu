@@ -216,8 +216,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
   constexpr int KW = KB / 4;                 // TMEM words per key
   constexpr int VW = HAS_V ? (VB == 8 ? 2 : 1) : 0;  // TMEM words per value
   constexpr int NW = KW + VW;                // stashed words per item: key (+ value)
-  constexpr bool CPAIRS = OS_COUNT_PAIRS && kCounterBytes == 2 && THREADS * 2 >= kMaxRadix &&
-                         TILE * KB < 65536;  // (a digit's packed tile total must stay below 2^16)
+  constexpr bool CPAIRS = OS_COUNT_PAIRS && kCounterBytes == 2 && THREADS * 2 >= kMaxRadix;
+  // a digit's scaled tile total can reach 2^16 (8192 x 8 B tiles): sum the
+  // two halves separately and mask the packed offsets
+  constexpr bool WIDEPAIR = TILE * KB >= 65536;
   // u32 keys with u32 values, both stashed: the reorder writes (key, value)
   // pairs into the key + value buffers viewed as one 8-byte-slot array (one
   // STS.64 per item instead of two scattered STS.32), the run writes read
@@ -618,14 +620,24 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
     uint32_t wk[WARPS];
     uint32_t c0 = 0, c1 = 0;
     if (owner) {
-      uint32_t sum = 0;
+      uint32_t sum = 0, sum_hi = 0;
 #pragma unroll
       for (int w = 0; w < WARPS; ++w) {
         wk[w] = w32[w * (kMaxRadix / 2) + tid];
-        sum += wk[w];
+        if constexpr (WIDEPAIR) {
+          sum += wk[w] & 0xffffu;
+          sum_hi += wk[w] >> 16;
+        } else {
+          sum += wk[w];
+        }
       }
-      c0 = (sum & 0xffffu) / KB;
-      c1 = (sum >> 16) / KB;
+      if constexpr (WIDEPAIR) {
+        c0 = sum / KB;
+        c1 = sum_hi / KB;
+      } else {
+        c0 = (sum & 0xffffu) / KB;
+        c1 = (sum >> 16) / KB;
+      }
       if (d0 == radix - 1) c0 -= uint32_t(TILE) - valid;
       if (d1 == radix - 1) c1 -= uint32_t(TILE) - valid;
       if (P.rts_offsets == nullptr) {  // (reduce-then-scan passes have no look-back)
@@ -658,12 +670,22 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
       if (has1) s_local[d1] = ls1 | (c1 << 16);
       // fold the tile-local starts into every warp's counters, so the
       // reorder needs a single shared-memory gather per key
-      uint32_t run = (ls0 * KB) | ((ls1 * KB) << 16);
       uint32_t* o32 = reinterpret_cast<uint32_t*>(s_whist);
+      if constexpr (WIDEPAIR) {
+        uint32_t run0 = ls0 * KB, run1 = ls1 * KB;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        o32[w * (kMaxRadix / 2) + tid] = run;
-        run += wk[w];
+        for (int w = 0; w < WARPS; ++w) {  // (an unused entry may reach 2^16: masked)
+          o32[w * (kMaxRadix / 2) + tid] = (run0 & 0xffffu) | (run1 << 16);
+          run0 += wk[w] & 0xffffu;
+          run1 += wk[w] >> 16;
+        }
+      } else {
+        uint32_t run = (ls0 * KB) | ((ls1 * KB) << 16);
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+          o32[w * (kMaxRadix / 2) + tid] = run;
+          run += wk[w];
+        }
       }
     }
   } else {
