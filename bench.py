@@ -382,7 +382,7 @@ def run_ours(args) -> None:
             # moves its 1 GiB in and its 1 GiB out over PCIe)
             from paper_2206_01784_b200 import SortPipeline
 
-            depth = 3  # tools/pipe_probe.py: 24.3 / 23.3 / 23.3 ms per step at depth 2 / 3 / 4
+            depth = 4  # tools/pipe_probe.py: 24.3 / 23.3 / 23.3 and 31.0 / 25.7 / 23.9 ms per step at depth 2 / 3 / 4 (two boxes)
             pipe = SortPipeline(n, torch.uint32, depth=depth)
             outs_h = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(depth)]
             for j in range(depth):  # warm-up
