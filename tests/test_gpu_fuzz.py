@@ -150,3 +150,25 @@ def test_fuzz(cuda, oracle, case):
         assert got_v.dtype == vals.dtype
         assert np.array_equal(np.ascontiguousarray(got_v).view(np.uint8),
                               np.ascontiguousarray(want_v).view(np.uint8)), case
+
+
+@pytest.mark.parametrize("case", [c for c in _cases() if c["begin"] == 0 and c["end"] == np.dtype(c["dt"]).itemsize * 8][::4],
+                         ids=lambda c: f"{c['i']}-{np.dtype(c['dt']).name}-{c['n']}-{c['dist']}")
+def test_fuzz_rts(cuda, oracle, case):
+    """The reduce-then-scan comparator (baseline.py:121-173) over the same draws."""
+    from paper_2206_01784_b200 import radix_plan, rts_sort
+
+    rng = np.random.default_rng(SEED * 1000 + case["i"])
+    dt, n = case["dt"], case["n"]
+    keys = _keys(rng, dt, n, case["dist"])
+    vals = _values(rng, case["vdt"], n)
+    cfg = radix_plan(np.dtype(dt).itemsize * 8, case["digit_bits"])
+    want = oracle.stable_sort_bits(keys, vals)
+    want_k, want_v = (want, None) if vals is None else want
+    got = rts_sort(keys, vals, cfg=cfg)
+    got_k, got_v = (got, None) if vals is None else got
+    u = _uint(dt)
+    assert np.array_equal(got_k.view(u), want_k.view(u)), case
+    if vals is not None:
+        assert np.array_equal(np.ascontiguousarray(got_v).view(np.uint8),
+                              np.ascontiguousarray(want_v).view(np.uint8)), case
