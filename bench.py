@@ -385,7 +385,7 @@ def run_ours(args) -> None:
             depth = 4  # tools/pipe_probe.py: 24.3 / 23.3 / 23.3 and 31.0 / 25.7 / 23.9 ms per step at depth 2 / 3 / 4 (two boxes)
             pipe = SortPipeline(n, torch.uint32, depth=depth)
             outs_h = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(depth)]
-            for j in range(depth):  # warm-up
+            for j in range(2 * depth):  # warm-up: every slot's sort runs once and is captured as a graph
                 pipe.submit(keys_h, outs_h[j % depth])
             pipe.synchronize()
             # pipeline fill and drain are inside the timing; 48 steps amortise
