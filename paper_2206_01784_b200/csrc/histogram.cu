@@ -206,6 +206,33 @@ __global__ void __launch_bounds__(kHistThreads, 1) onesweep_histogram_kernel(con
   if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, P.passes, s_trivial, P.fixed_ends != 0);
 }
 
+// Last block's scan for 8-bit places: the 1024 threads take four places per
+// round (thread t: place p0 + t / 256, digit t % 256), so every place's
+// counts are fetched from L2 in one round trip instead of one per place.
+__device__ __forceinline__ void scan_places256(const HistParams& P, int places,
+                                               unsigned long long* s_wsum, uint32_t* s_trivial) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = tid >> 8;  // place within the round
+  for (int p0 = 0; p0 < places; p0 += kHistThreads / 256) {
+    const int p = p0 + q;
+    const unsigned long long x = p < places ? __ldcg(&P.hist[p * 256 + (tid & 255)]) : 0ull;
+    if (p < places && x == P.n) atomicOr(s_trivial, 1u << p);  // one bin holds every key
+    unsigned long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    unsigned long long pre = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) pre += (w < (warp & 7)) ? s_wsum[(warp & ~7) + w] : 0ull;
+    if (p < places) P.offsets[p * 256 + (tid & 255)] = pre + incl - x;
+    __syncthreads();
+  }
+}
+
 // Specialisation for the headline shape: 32-bit keys, four byte-aligned
 // 8-bit places (begin_bit 0, end_bit 32).  Counters are lane-private u32
 // (4 places x 256 digits x 32 lanes = 128 KiB, bank = lane: conflict-free and
@@ -297,22 +324,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int p = 0; p < 4; ++p) {
-    const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
-    if (tid < 256 && x == P.n) atomicOr(&s_trivial, 1u << p);  // one bin holds every key
-    unsigned long long incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_wsum[warp] = incl;
-    __syncthreads();
-    unsigned long long pre = 0;
-    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
-    if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
-    __syncthreads();
-  }
+  scan_places256(P, 4, s_wsum, &s_trivial);
   if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, 4, s_trivial, P.fixed_ends != 0);
 }
 
@@ -429,22 +441,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int p = 0; p < 8; ++p) {
-    const unsigned long long x = (tid < 256) ? __ldcg(&P.hist[p * 256 + tid]) : 0ull;
-    if (tid < 256 && x == P.n) atomicOr(&s_trivial, 1u << p);  // one bin holds every key
-    unsigned long long incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_wsum[warp] = incl;
-    __syncthreads();
-    unsigned long long pre = 0;
-    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
-    if (tid < 256) P.offsets[p * 256 + tid] = pre + incl - x;
-    __syncthreads();
-  }
+  scan_places256(P, 8, s_wsum, &s_trivial);
   if (tid == 0 && P.tickets != nullptr) plan_tickets(P.tickets, P.ticket_stride, P.strips, 8, s_trivial, P.fixed_ends != 0);
 }
 
