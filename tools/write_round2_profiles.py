@@ -9,6 +9,7 @@ import csv
 import gzip
 import io
 import json
+import os
 import shutil
 import sys
 
@@ -130,16 +131,26 @@ open(f"{P}/round2_ncu_summary.md", "w").write(md)
 for s, d in [(f"bench_{tag}.json", "round2_bench.json"), (f"bench_{tag}_ref.json", "round2_bench_reference.json"),
              (f"launches_{tag}.csv", "round2_launches.csv"), (f"cfgs_{tag}.jsonl", "round2_configs.jsonl"),
              (f"reference_suite_{tag}.log", "round2_reference_suite.txt")]:
+    if d == "round2_reference_suite.txt" and "rc=0" not in open(f"{G}/{s}").read() if os.path.exists(f"{G}/{s}") else False:
+        print("reference suite did not pass in this session:", s, "(kept the committed file)")
+        continue
     try:
         shutil.copy(f"{G}/{s}", f"{P}/{d}")
     except FileNotFoundError:
         print("missing", s)
-with open(f"{P}/round2_sanitize.txt", "w") as out:
-    for tool in ("memcheck", "racecheck", "synccheck", "initcheck"):
-        try:
-            lines = open(f"{G}/sanitize_{tool}_{tag}.log").read().splitlines()
-        except FileNotFoundError:
-            continue
-        keep = [ln for ln in lines if ln.startswith("case ok") or "SUMMARY" in ln or "SANITIZE" in ln]
-        out.write(f"== compute-sanitizer --tool {tool} python tools/sanitize_cases.py\n" + "\n".join(keep) + "\n\n")
+san = {}
+for tool in ("memcheck", "racecheck", "synccheck", "initcheck"):
+    try:
+        lines = open(f"{G}/sanitize_{tool}_{tag}.log").read().splitlines()
+    except FileNotFoundError:
+        continue
+    keep = [ln for ln in lines if ln.startswith("case ok") or "SUMMARY" in ln or "SANITIZE" in ln]
+    if any("SUMMARY" in ln for ln in keep):  # (a refused run, e.g. the pool closed the tool, keeps the last file)
+        san[tool] = keep
+if san:
+    with open(f"{P}/round2_sanitize.txt", "w") as out:
+        for tool, keep in san.items():
+            out.write(f"== compute-sanitizer --tool {tool} python tools/sanitize_cases.py  (session {tag})\n" + "\n".join(keep) + "\n\n")
+else:
+    print("no sanitizer summaries in this session: profiles/round2_sanitize.txt kept")
 print(open(f"{P}/round2_ncu_summary.md").read())
