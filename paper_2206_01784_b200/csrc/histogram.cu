@@ -250,7 +250,6 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   __shared__ uint32_t s_trivial;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int warp = tid >> 5;
   {
     uint4* z = reinterpret_cast<uint4*>(s_cnt);
     for (int i = tid; i < int(kHistU32Smem / 16); i += kHistThreads) z[i] = make_uint4(0, 0, 0, 0);
@@ -351,7 +350,6 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   __shared__ uint32_t s_trivial;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int warp = tid >> 5;
   const uint32_t raw = smem_u32(s_raw);
   const uint32_t tbase = (raw + 32767u) & ~32767u;  // counter table, 32 KiB-aligned
   uint32_t* s_tab = reinterpret_cast<uint32_t*>(s_raw + (tbase - raw));
