@@ -75,8 +75,12 @@ constexpr int kLookbackWindow = OS_LOOKBACK_WINDOW;
 // bit 1: leader write -> next read; one NOP each).  Timing (round 2, 10K
 // tiles, 3 interleaved runs): both 686 us, none 728; with the key prefetch
 // both 659, none 705 -- the NOPs pay for themselves in the warp schedule.
+// The read -> leader-write order is also a data dependency (the leader
+// stores the rank its own load returned, and a converged warp's load returns
+// for every lane at once), so bit 0 is redundant; bit 1 alone (session r2j,
+// 3 interleaved runs): C2 663.0 -> 659.3 us/pass.
 #ifndef OS_SYNCWARP
-#define OS_SYNCWARP 3
+#define OS_SYNCWARP 2
 #endif
 
 // Skip the multisplit for warps whose 32*ITEMS keys share one digit.
