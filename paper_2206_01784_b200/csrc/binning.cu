@@ -173,10 +173,11 @@ __device__ __forceinline__ void jitter_sleep(uint32_t tile, uint32_t lane_id, ui
 #ifndef OS_COUNT_PAIRS
 #define OS_COUNT_PAIRS 1  // the count phase works on digit pairs (one 32-bit counter word per thread)
 #endif
-// u32 key + u32 value passes: a __syncwarp() every k-th run-write slot
-// paces each warp's LDS.64 / STG pairs (session r2k, C3 q=1 / q=4 / q=16:
+// u32 keys with values: a __syncwarp() every k-th run-write slot paces each
+// warp's loads / two stores per slot (session r2k, C3 q=1 / q=4 / q=16:
 // 1024 / 949 / 805 -> 999 / 922 / 803 us/pass at k = 3; k = 1 loses at
-// q=16, and the other kernels do not gain: profiles/round2_binning_notes.md)
+// q=16; u32 keys + 1 / 2 / 8-byte values +0.4 / +1.9 / +1.4 %; keys-only and
+// u64-key kernels do not gain: profiles/round2_binning_notes.md)
 #ifndef OS_PAIR_WRITE_FENCE
 #define OS_PAIR_WRITE_FENCE 3
 #endif
@@ -970,8 +971,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         write_slot(uint32_t(j * THREADS + tid));
-        // (u32 pairs: a warp fence every OS_PAIR_WRITE_FENCE slots, see its definition)
-        if (PAIRS && OS_PAIR_WRITE_FENCE > 0 && j % (OS_PAIR_WRITE_FENCE > 0 ? OS_PAIR_WRITE_FENCE : 1) == 0)
+        // (u32 keys with values: a warp fence every OS_PAIR_WRITE_FENCE slots, see its definition)
+        if (HAS_V && KB == 4 && OS_PAIR_WRITE_FENCE > 0 &&
+            j % (OS_PAIR_WRITE_FENCE > 0 ? OS_PAIR_WRITE_FENCE : 1) == 0)
           __syncwarp();
       }
     } else {
