@@ -975,6 +975,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_binning_kernel(const P
         if (HAS_V && KB == 4 && OS_PAIR_WRITE_FENCE > 0 &&
             j % (OS_PAIR_WRITE_FENCE > 0 ? OS_PAIR_WRITE_FENCE : 1) == 0)
           __syncwarp();
+        // (u64 keys with 8-byte values: every second slot, 18.34 -> 18.65 GKey/s)
+        if (HAS_V && KB == 8 && VB == 8 && j % 2 == 0) __syncwarp();
       }
     } else {
       for (uint32_t s = tid; s < valid; s += THREADS) write_slot(s);
